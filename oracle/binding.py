@@ -1,0 +1,343 @@
+"""ctypes bindings for the oracle -- TEST INFRASTRUCTURE ONLY.
+
+Loaded only by tests/, __graft_entry__.smoke() and bench.py's CPU-baseline /
+``--impl reference`` legs.  Two libraries:
+
+* ``liboracle.so``   -- plain-C restatement of the reference (oracle.c).
+* ``_ref/libtrigraph_ref.so`` -- the unmodified reference headers behind a
+  C shim (ref_shim.cpp); present wherever `make -C oracle` ran with
+  /root/reference mounted (it then travels to the GPU box as a built file).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+U64, U32, F64 = np.uint64, np.uint32, np.float64
+P = C.c_void_p
+
+ENGINES = {"seq": 0, "aop": 1, "anop-direct": 2, "anop-surrogate": 3}
+COSTS = {"N": 0, "D": 1, "DH": 2, "DDH": 3, "DH2": 4, "DPD": 5, "NOV": 6}
+
+_orc = None
+_ref = None
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(P)
+
+
+def lib():
+    global _orc
+    if _orc is None:
+        path = os.path.join(HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"oracle not built: {path} (run make -C oracle)")
+        L = C.CDLL(path)
+        u64, vp, i32, dbl = C.c_uint64, C.c_void_p, C.c_int, C.c_double
+        sig = {
+            "orc_build_graph": (u64, [vp, u64, u64, C.POINTER(vp), C.POINTER(vp)]),
+            "orc_free": (None, [vp]),
+            "orc_degree_rank": (None, [u64, vp, vp]),
+            "orc_effective": (u64, [u64, vp, vp, vp, vp, C.POINTER(vp)]),
+            "orc_count": (u64, [u64, vp, vp, vp, vp, u64]),
+            "orc_ordering_cost": (u64, [u64, vp, vp, vp]),
+            "orc_node_costs": (None, [u64, vp, vp, vp, vp, i32, vp, vp]),
+            "orc_compute_boundaries": (i32, [vp, u64, u64, vp]),
+            "orc_owner": (u64, [vp, u64, C.c_uint32]),
+            "orc_run_engine": (u64, [u64, vp, vp, i32, u64, i32, vp, vp, vp, vp, vp,
+                                     vp, vp, vp, u64]),
+            "orc_cc": (None, [u64, vp, vp, vp]),
+            "orc_random_graph_pairs": (u64, [u64, dbl, u64, vp, u64]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _orc = L
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(HERE, "_ref", "libtrigraph_ref.so"))
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        path = os.path.join(HERE, "_ref", "libtrigraph_ref.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"reference shim not built: {path}")
+        L = C.CDLL(path)
+        u64, vp, i32, dbl = C.c_uint64, C.c_void_p, C.c_int, C.c_double
+        sig = {
+            "ref_graph_from_pairs": (vp, [vp, u64, u64]),
+            "ref_graph_from_csr": (vp, [u64, vp, vp]),
+            "ref_random_graph": (vp, [u64, dbl, u64]),
+            "ref_complete": (vp, [u64]),
+            "ref_wheel": (vp, [u64]),
+            "ref_complete_bipartite": (vp, [u64, u64]),
+            "ref_g5": (vp, []),
+            "ref_gen_pa": (vp, [u64, u64, u64]),
+            "ref_gen_gnp": (vp, [u64, dbl, u64]),
+            "ref_graph_free": (None, [vp]),
+            "ref_num_nodes": (u64, [vp]),
+            "ref_num_edges": (u64, [vp]),
+            "ref_graph_csr": (None, [vp, vp, vp]),
+            "ref_degree_rank": (None, [vp, vp]),
+            "ref_effective": (u64, [vp, vp, vp]),
+            "ref_count": (u64, [vp]),
+            "ref_ordering_cost": (u64, [vp]),
+            "ref_node_costs": (None, [vp, i32, vp, vp]),
+            "ref_compute_boundaries": (i32, [vp, u64, u64, vp]),
+            "ref_overlap_stored": (u64, [vp, vp, u64, u64]),
+            "ref_run_engine": (u64, [vp, i32, u64, i32, vp, vp, vp, vp, vp, vp, vp, u64,
+                                     vp, i32]),
+            "ref_clustering": (i32, [vp, i32, u64, i32, vp, vp]),
+            "ref_time_sequential": (dbl, [vp, vp]),
+            "ref_prepare": (None, [vp]),
+            "ref_aop_sample": (dbl, [vp, u64, vp, u64, i32, vp, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _ref = L
+    return _ref
+
+
+# ---------------------------------------------------------------- oracle API
+
+
+@dataclass
+class CSR:
+    n: int
+    off: np.ndarray  # uint64[n+1]
+    adj: np.ndarray  # uint32[2m]
+
+    @property
+    def m(self) -> int:
+        return int(self.off[-1]) // 2
+
+
+def build_graph(pairs, n_override: int = 0) -> CSR:
+    """graph.hpp:58-85 via the C restatement."""
+    pairs = np.ascontiguousarray(np.asarray(pairs, dtype=U32).reshape(-1, 2))
+    L = lib()
+    po, pa = C.c_void_p(), C.c_void_p()
+    n = L.orc_build_graph(_ptr(pairs), pairs.shape[0], n_override, C.byref(po), C.byref(pa))
+    off = np.ctypeslib.as_array(C.cast(po, C.POINTER(C.c_uint64)), (n + 1,)).copy()
+    m2 = int(off[-1])
+    adj = (np.ctypeslib.as_array(C.cast(pa, C.POINTER(C.c_uint32)), (max(m2, 1),))[:m2].copy())
+    L.orc_free(po)
+    L.orc_free(pa)
+    return CSR(int(n), off, adj)
+
+
+def degree_rank(g: CSR) -> np.ndarray:
+    r = np.zeros(g.n, dtype=U32)
+    lib().orc_degree_rank(g.n, _ptr(g.off), _ptr(r))
+    return r
+
+
+def effective(g: CSR):
+    rank = degree_rank(g)
+    eoff = np.zeros(g.n + 1, dtype=U64)
+    pe = C.c_void_p()
+    m = lib().orc_effective(g.n, _ptr(g.off), _ptr(g.adj), _ptr(rank), _ptr(eoff), C.byref(pe))
+    eff = np.ctypeslib.as_array(C.cast(pe, C.POINTER(C.c_uint32)), (max(m, 1),))[:m].copy()
+    lib().orc_free(pe)
+    return eoff, eff
+
+
+def count(g: CSR, tally=False, listing=False):
+    eoff, eff = effective(g)
+    L = lib()
+    T = L.orc_count(g.n, _ptr(eoff), _ptr(eff), None, None, 0)
+    tv = np.zeros(g.n, dtype=U64) if tally else None
+    tri = np.zeros((max(T, 1), 3), dtype=U32) if listing else None
+    if tally or listing:
+        L.orc_count(g.n, _ptr(eoff), _ptr(eff), _ptr(tv), _ptr(tri), T)
+    if listing:
+        tri = tri[:T]
+        tri = tri[np.lexsort((tri[:, 2], tri[:, 1], tri[:, 0]))]
+    return int(T), tv, tri
+
+
+def ordering_cost(g: CSR) -> int:
+    return int(lib().orc_ordering_cost(g.n, _ptr(g.off), _ptr(g.adj), _ptr(degree_rank(g))))
+
+
+def node_costs(g: CSR, kind: str):
+    eoff, eff = effective(g)
+    f = np.zeros(g.n, dtype=U64)
+    pre = np.zeros(g.n, dtype=U64)
+    lib().orc_node_costs(g.n, _ptr(g.off), _ptr(g.adj), _ptr(eoff), _ptr(eff), COSTS[kind],
+                         _ptr(f), _ptr(pre))
+    return f, pre
+
+
+def compute_boundaries(f, p: int):
+    f = np.asarray(f, dtype=U64)
+    pre = np.cumsum(f, dtype=U64) if len(f) else np.zeros(0, dtype=U64)
+    b = np.zeros(p + 1, dtype=U32)
+    if lib().orc_compute_boundaries(_ptr(pre), len(f), p, _ptr(b)) != 0:
+        raise ValueError("compute_boundaries: p must be >= 1")
+    return b
+
+
+@dataclass
+class Report:
+    total: int
+    boundaries: np.ndarray
+    triangles: np.ndarray
+    data_sent: np.ndarray
+    data_recv: np.ndarray
+    stored: np.ndarray
+    node_counts: np.ndarray | None = None
+    triangles_list: np.ndarray | None = None
+
+
+def run_engine(g: CSR, engine="aop", ranks=1, cost="DPD", boundaries=None,
+               track_nodes=False, collect_triangles=False) -> Report:
+    """engines.hpp:335-418 run_engine via the C restatement."""
+    e = ENGINES[engine]
+    p = 1 if engine == "seq" else int(ranks)
+    if p == 0:
+        raise ValueError("run_engine: ranks must be >= 1")
+    L = lib()
+    bo = np.zeros(p + 1, dtype=U32)
+    bi = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=U32)
+    tri, sent, recv, st = (np.zeros(p, dtype=U64) for _ in range(4))
+    tv = np.zeros(g.n, dtype=U64) if track_nodes else None
+    T, _, _ = count(g) if collect_triangles else (0, None, None)
+    lst = np.zeros((max(T, 1), 3), dtype=U32) if collect_triangles else None
+    total = L.orc_run_engine(g.n, _ptr(g.off), _ptr(g.adj), e, p, COSTS[cost], _ptr(bi),
+                             _ptr(bo), _ptr(tri), _ptr(sent), _ptr(recv), _ptr(st),
+                             _ptr(tv), _ptr(lst), T)
+    if collect_triangles:
+        lst = lst[:T]
+        lst = lst[np.lexsort((lst[:, 2], lst[:, 1], lst[:, 0]))]
+    return Report(int(total), bo, tri, sent, recv, st, tv, lst)
+
+
+def clustering(g: CSR, tv) -> np.ndarray:
+    c = np.zeros(g.n, dtype=F64)
+    lib().orc_cc(g.n, _ptr(g.off), _ptr(np.ascontiguousarray(tv, dtype=U64)), _ptr(c))
+    return c
+
+
+def random_graph_pairs(n: int, density: float, seed: int) -> np.ndarray:
+    """proj/tests/oracles.hpp:49-57 random_graph's accepted pairs."""
+    cap = n * (n - 1) // 2
+    out = np.zeros((max(cap, 1), 2), dtype=U32)
+    c = lib().orc_random_graph_pairs(n, density, seed, _ptr(out), cap)
+    return out[:c]
+
+
+def random_graph(n: int, density: float, seed: int) -> CSR:
+    return build_graph(random_graph_pairs(n, density, seed), n)
+
+
+# --------------------------------------------------- reference (oracle/_ref)
+
+
+class RefGraph:
+    """Owns a reference trigraph::Graph built by the unmodified headers."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_graph_free(self.h)
+            self.h = None
+
+    @property
+    def n(self) -> int:
+        return int(ref().ref_num_nodes(self.h))
+
+    @property
+    def m(self) -> int:
+        return int(ref().ref_num_edges(self.h))
+
+    def csr(self) -> CSR:
+        n, m = self.n, self.m
+        off = np.zeros(n + 1, dtype=U64)
+        adj = np.zeros(max(2 * m, 1), dtype=U32)
+        ref().ref_graph_csr(self.h, _ptr(off), _ptr(adj))
+        return CSR(n, off, adj[: 2 * m])
+
+    @classmethod
+    def from_pairs(cls, pairs, n_override=0):
+        pairs = np.ascontiguousarray(np.asarray(pairs, dtype=U32).reshape(-1, 2))
+        return cls(ref().ref_graph_from_pairs(_ptr(pairs), pairs.shape[0], n_override))
+
+    @classmethod
+    def from_csr(cls, g: CSR):
+        return cls(ref().ref_graph_from_csr(g.n, _ptr(g.off), _ptr(g.adj)))
+
+    def degree_rank(self):
+        r = np.zeros(self.n, dtype=U32)
+        ref().ref_degree_rank(self.h, _ptr(r))
+        return r
+
+    def effective(self):
+        m = int(ref().ref_effective(self.h, None, None))
+        eoff = np.zeros(self.n + 1, dtype=U64)
+        eff = np.zeros(max(m, 1), dtype=U32)
+        ref().ref_effective(self.h, _ptr(eoff), _ptr(eff))
+        return eoff, eff[:m]
+
+    def count(self) -> int:
+        return int(ref().ref_count(self.h))
+
+    def ordering_cost(self) -> int:
+        return int(ref().ref_ordering_cost(self.h))
+
+    def node_costs(self, kind: str):
+        f = np.zeros(self.n, dtype=U64)
+        pre = np.zeros(self.n, dtype=U64)
+        ref().ref_node_costs(self.h, COSTS[kind], _ptr(f), _ptr(pre))
+        return f, pre
+
+    def overlap_stored(self, b, i):
+        b = np.ascontiguousarray(b, dtype=U32)
+        return int(ref().ref_overlap_stored(self.h, _ptr(b), len(b) - 1, i))
+
+    def run_engine(self, engine="aop", ranks=1, cost="DPD", boundaries=None,
+                   track_nodes=False, collect_triangles=False, concurrent=False):
+        e = ENGINES[engine]
+        p = 1 if engine == "seq" else int(ranks)
+        bo = np.zeros(max(p, 1) + 1, dtype=U32)
+        bi = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=U32)
+        tri, sent, recv = (np.zeros(max(p, 1), dtype=U64) for _ in range(3))
+        tv = np.zeros(self.n, dtype=U64) if track_nodes else None
+        cap = self.count() if collect_triangles else 0
+        lst = np.zeros((max(cap, 1), 3), dtype=U32) if collect_triangles else None
+        nl = np.zeros(1, dtype=U64)
+        total = ref().ref_run_engine(self.h, e, int(ranks), COSTS[cost], _ptr(bi), _ptr(bo),
+                                     _ptr(tri), _ptr(sent), _ptr(recv), _ptr(tv), _ptr(lst),
+                                     cap, _ptr(nl), 1 if concurrent else 0)
+        if total == 2**64 - 1:
+            raise ValueError("run_engine: ranks must be >= 1")
+        return Report(int(total), bo, tri, sent, recv, np.zeros(p, dtype=U64), tv,
+                      None if lst is None else lst[: int(nl[0])])
+
+    def clustering(self, engine="aop", ranks=1, cost="DPD"):
+        tv = np.zeros(self.n, dtype=U64)
+        c = np.zeros(self.n, dtype=F64)
+        if ref().ref_clustering(self.h, ENGINES[engine], ranks, COSTS[cost], _ptr(tv),
+                                _ptr(c)) != 0:
+            raise ValueError("clustering_coefficients: ranks must be >= 1")
+        return tv, c
+
+
+def ref_random_graph(n, density, seed) -> RefGraph:
+    return RefGraph(ref().ref_random_graph(n, density, seed))
+
+
+def ref_fixture(name: str, *args) -> RefGraph:
+    return RefGraph(getattr(ref(), "ref_" + name)(*args))

@@ -1,0 +1,101 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference `trigraph` hot path
+ * (/root/reference/proj/include/trigraph/*.hpp), used as the parity checker
+ * for the B200 library.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it.  The product path
+ * (paper_1706_05151_b200/) never links or calls anything in this directory.
+ *
+ * Pinning: the restatement is checked against the reference itself, built
+ * from its own headers into oracle/_ref/ (see oracle/Makefile, ref_shim.cpp),
+ * and against the reference tests' golden vectors (tests/golden/).
+ *
+ * Conventions: NodeId = uint32_t, offsets are uint64_t (reference size_t),
+ * counters are uint64_t (reference std::uint64_t).
+ */
+#ifndef TG_ORACLE_H
+#define TG_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* graph.hpp:58-85 build_graph.  pairs = E (u,v) pairs, interleaved.
+ * Returns n; *off_out (n+1) and *adj_out (2m) are malloc'ed (orc_free). */
+uint64_t orc_build_graph(const uint32_t* pairs, uint64_t E, uint64_t n_override,
+                         uint64_t** off_out, uint32_t** adj_out);
+void orc_free(void* p);
+
+/* order.hpp:95-104 compute_order(ByDegree): rank[v] = position of v in the
+ * (degree, id) ascending sort. */
+void orc_degree_rank(uint64_t n, const uint64_t* off, uint32_t* rank);
+
+/* effective.hpp:37-52.  eoff has n+1 entries (caller-allocated);
+ * *eff_out (m entries) malloc'ed.  Returns m. */
+uint64_t orc_effective(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                       const uint32_t* rank, uint64_t* eoff, uint32_t** eff_out);
+
+/* sequential.hpp:74-91 count_node_iterator_n, with NodeTallySink
+ * (sequential.hpp:24-33, tally may be NULL) and ListSink (sequential.hpp:36-46,
+ * tri may be NULL; at most tri_cap triples written, normalised ascending). */
+uint64_t orc_count(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
+                   uint64_t* tally, uint32_t* tri, uint64_t tri_cap);
+
+/* sequential.hpp:95-104 ordering_cost under the degree order. */
+uint64_t orc_ordering_cost(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                           const uint32_t* rank);
+
+/* partition.hpp:18 CostKind, in declaration order. */
+enum { ORC_COST_N = 0, ORC_COST_D, ORC_COST_DH, ORC_COST_DDH, ORC_COST_DH2,
+       ORC_COST_DPD, ORC_COST_NOV };
+
+/* partition.hpp:45-91 node_costs (EffectiveOnly DPD variant). */
+void orc_node_costs(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                    const uint64_t* eoff, const uint32_t* eff, int kind,
+                    uint64_t* f, uint64_t* prefix);
+
+/* partition.hpp:116-141 compute_boundaries; b has p+1 entries.
+ * Returns 0, or -1 when p == 0 (reference: std::invalid_argument). */
+int orc_compute_boundaries(const uint64_t* prefix, uint64_t n, uint64_t p,
+                           uint32_t* b);
+
+/* partition.hpp:106-109 PartitionPlan::owner. */
+uint64_t orc_owner(const uint32_t* b, uint64_t p, uint32_t v);
+
+/* engines.hpp:24 EngineKind, in declaration order. */
+enum { ORC_ENGINE_SEQ = 0, ORC_ENGINE_AOP, ORC_ENGINE_ANOP_DIRECT,
+       ORC_ENGINE_ANOP_SURROGATE };
+
+/* engines.hpp:335-418 run_engine (degree order).  boundaries_in may be NULL
+ * (cost-based plan).  boundaries_out has p+1 entries; tri/sent/recv/stored
+ * have p entries each (stored = partition stored_entries()).  tally (n) and
+ * list (3*list_cap) may be NULL.  Returns the global total, or UINT64_MAX on
+ * invalid arguments (ranks == 0). */
+uint64_t orc_run_engine(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                        int engine, uint64_t p, int cost,
+                        const uint32_t* boundaries_in, uint32_t* boundaries_out,
+                        uint64_t* tri, uint64_t* sent, uint64_t* recv,
+                        uint64_t* stored, uint64_t* tally, uint32_t* list,
+                        uint64_t list_cap);
+
+/* engines.hpp:422-435 clustering coefficient formula. */
+void orc_cc(uint64_t n, const uint64_t* off, const uint64_t* tally, double* c);
+
+/* proj/tests/oracles.hpp:49-57 random_graph(n, density, seed): writes the
+ * accepted (u,v) pairs into out (2*cap uint32); returns the pair count
+ * (which may exceed cap, in which case only cap pairs were written). */
+uint64_t orc_random_graph_pairs(uint64_t n, double density, uint64_t seed,
+                                uint32_t* out, uint64_t cap);
+
+/* std::mt19937_64 restated (used by the fixture generators). */
+typedef struct { uint64_t mt[312]; int mti; } orc_mt64;
+void orc_mt64_seed(orc_mt64* s, uint64_t seed);
+uint64_t orc_mt64_next(orc_mt64* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,265 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C-ABI shim over the UNMODIFIED reference headers
+// (/root/reference/proj/include/trigraph/*.hpp and proj/tests/oracles.hpp),
+// compiled by oracle/Makefile into oracle/_ref/libtrigraph_ref.so.  Nothing
+// from the reference is copied: the headers are used in place through -I.
+//
+// Uses: (1) pinning the C restatement in oracle.c and the B200 library
+// against the reference itself; (2) generating tests/golden/ fixtures;
+// (3) the CPU baseline / `bench.py --impl reference` arm, which times the
+// reference's own NodeIteratorN and AOP rank bodies on the host cores.
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "oracles.hpp"
+#include "trigraph/trigraph.hpp"
+
+using namespace trigraph;
+
+namespace {
+
+struct RefGraph {
+  Graph g;
+  std::optional<OrderRank> order;
+  std::optional<EffectiveAdjacency> eff;
+
+  const EffectiveAdjacency& effective() {
+    if (!eff) {
+      order = compute_order(g, OrderKind::by_degree());
+      eff = effective_adjacency(g, *order);
+    }
+    return *eff;
+  }
+};
+
+RefGraph* wrap(Graph g) {
+  auto* r = new RefGraph;
+  r->g = std::move(g);
+  return r;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
+
+extern "C" {
+
+void* ref_graph_from_pairs(const uint32_t* pairs, uint64_t E, uint64_t n_override) {
+  std::vector<std::pair<NodeId, NodeId>> e(E);
+  for (uint64_t i = 0; i < E; ++i) e[i] = {pairs[2 * i], pairs[2 * i + 1]};
+  return wrap(build_graph(e, n_override));
+}
+
+void* ref_graph_from_csr(uint64_t n, const uint64_t* off, const uint32_t* adj) {
+  std::vector<std::size_t> o(off, off + n + 1);
+  std::vector<NodeId> a(adj, adj + off[n]);
+  return wrap(Graph(n, std::move(o), std::move(a)));
+}
+
+void* ref_random_graph(uint64_t n, double density, uint64_t seed) {
+  return wrap(oracles::random_graph(n, density, seed));
+}
+void* ref_complete(uint64_t n) { return wrap(oracles::complete(n)); }
+void* ref_wheel(uint64_t rim) { return wrap(oracles::wheel(rim)); }
+void* ref_complete_bipartite(uint64_t a, uint64_t b) {
+  return wrap(oracles::complete_bipartite(a, b));
+}
+void* ref_g5() { return wrap(oracles::g5()); }
+void* ref_gen_pa(uint64_t n, uint64_t d, uint64_t seed) { return wrap(gen_pa(n, d, seed)); }
+void* ref_gen_gnp(uint64_t n, double d, uint64_t seed) { return wrap(gen_gnp(n, d, seed)); }
+
+void ref_graph_free(void* h) { delete static_cast<RefGraph*>(h); }
+
+uint64_t ref_num_nodes(void* h) { return static_cast<RefGraph*>(h)->g.num_nodes(); }
+uint64_t ref_num_edges(void* h) { return static_cast<RefGraph*>(h)->g.num_edges(); }
+
+void ref_graph_csr(void* h, uint64_t* off, uint32_t* adj) {
+  const Graph& g = static_cast<RefGraph*>(h)->g;
+  uint64_t k = 0;
+  off[0] = 0;
+  for (NodeId v = 0; v < g.num_nodes(); ++v) {
+    for (NodeId u : g.neighbors(v)) adj[k++] = u;
+    off[v + 1] = k;
+  }
+}
+
+void ref_degree_rank(void* h, uint32_t* rank) {
+  auto ord = compute_order(static_cast<RefGraph*>(h)->g, OrderKind::by_degree());
+  std::memcpy(rank, ord.rank.data(), ord.rank.size() * sizeof(uint32_t));
+}
+
+uint64_t ref_effective(void* h, uint64_t* eoff, uint32_t* eff) {
+  const auto& e = static_cast<RefGraph*>(h)->effective();
+  const uint64_t n = e.num_nodes();
+  uint64_t k = 0;
+  if (eoff) eoff[0] = 0;
+  for (NodeId v = 0; v < n; ++v) {
+    for (NodeId u : e.eff(v)) {
+      if (eff) eff[k] = u;
+      ++k;
+    }
+    if (eoff) eoff[v + 1] = k;
+  }
+  return k;
+}
+
+uint64_t ref_count(void* h) {
+  return count_node_iterator_n(static_cast<RefGraph*>(h)->effective());
+}
+
+uint64_t ref_ordering_cost(void* h) {
+  const Graph& g = static_cast<RefGraph*>(h)->g;
+  return ordering_cost(g, compute_order(g, OrderKind::by_degree()));
+}
+
+void ref_node_costs(void* h, int kind, uint64_t* f, uint64_t* prefix) {
+  auto* r = static_cast<RefGraph*>(h);
+  auto c = node_costs(r->g, r->effective(), static_cast<CostKind>(kind));
+  std::memcpy(f, c.f.data(), c.f.size() * sizeof(uint64_t));
+  std::memcpy(prefix, c.prefix.data(), c.prefix.size() * sizeof(uint64_t));
+}
+
+int ref_compute_boundaries(const uint64_t* f, uint64_t n, uint64_t p, uint32_t* b) {
+  CostVector c;
+  c.f.assign(f, f + n);
+  c.prefix.resize(n);
+  uint64_t acc = 0;
+  for (uint64_t i = 0; i < n; ++i) c.prefix[i] = (acc += f[i]);
+  try {
+    auto plan = compute_boundaries(c, p);
+    std::memcpy(b, plan.boundaries.data(), plan.boundaries.size() * sizeof(uint32_t));
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+}
+
+uint64_t ref_overlap_stored(void* h, const uint32_t* b, uint64_t p, uint64_t i) {
+  auto* r = static_cast<RefGraph*>(h);
+  PartitionPlan plan{std::vector<NodeId>(b, b + p + 1)};
+  return build_overlap_partition(r->g, r->effective(), plan, i).stored_entries();
+}
+
+// run_engine (engines.hpp:335).  tally != NULL turns on track_nodes; list !=
+// NULL turns on collect_triangles (sorted ascending, up to cap triples;
+// *n_listed gets the full count).  Returns total, UINT64_MAX on
+// std::invalid_argument.
+uint64_t ref_run_engine(void* h, int engine, uint64_t p, int cost, const uint32_t* b_in,
+                        uint32_t* b_out, uint64_t* tri, uint64_t* sent, uint64_t* recv,
+                        uint64_t* tally, uint32_t* list, uint64_t cap, uint64_t* n_listed,
+                        int concurrent) {
+  auto* r = static_cast<RefGraph*>(h);
+  EngineConfig cfg;
+  cfg.engine = static_cast<EngineKind>(engine);
+  cfg.ranks = p;
+  cfg.cost = static_cast<CostKind>(cost);
+  cfg.mode = concurrent ? runtime::ExecMode::Concurrent : runtime::ExecMode::Interleaved;
+  cfg.track_nodes = tally != nullptr;
+  cfg.collect_triangles = list != nullptr;
+  uint64_t pp = cfg.engine == EngineKind::Sequential ? 1 : p;
+  if (b_in) cfg.boundaries = std::vector<NodeId>(b_in, b_in + pp + 1);
+  RunReport rep;
+  try {
+    rep = run_engine(r->g, cfg);
+  } catch (const std::invalid_argument&) {
+    return UINT64_MAX;
+  }
+  std::memcpy(b_out, rep.boundaries.data(), rep.boundaries.size() * sizeof(uint32_t));
+  for (std::size_t i = 0; i < rep.per_rank.size(); ++i) {
+    tri[i] = rep.per_rank[i].triangles;
+    sent[i] = rep.per_rank[i].data_sent;
+    recv[i] = rep.per_rank[i].data_recv;
+  }
+  if (tally)
+    std::memcpy(tally, rep.node_counts.data(), rep.node_counts.size() * sizeof(uint64_t));
+  if (list) {
+    std::sort(rep.triangles_list.begin(), rep.triangles_list.end());
+    *n_listed = rep.triangles_list.size();
+    for (uint64_t k = 0; k < rep.triangles_list.size() && k < cap; ++k)
+      for (int c = 0; c < 3; ++c) list[3 * k + c] = rep.triangles_list[k][c];
+  }
+  return rep.total;
+}
+
+int ref_clustering(void* h, int engine, uint64_t p, int cost, uint64_t* tally, double* c) {
+  auto* r = static_cast<RefGraph*>(h);
+  EngineConfig cfg;
+  cfg.engine = static_cast<EngineKind>(engine);
+  cfg.ranks = p;
+  cfg.cost = static_cast<CostKind>(cost);
+  try {
+    auto cc = clustering_coefficients(r->g, cfg);
+    std::memcpy(tally, cc.triangles_per_node.data(), cc.triangles_per_node.size() * 8);
+    std::memcpy(c, cc.coefficient.data(), cc.coefficient.size() * 8);
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+  return 0;
+}
+
+// ---- CPU baseline legs (bench.py cpu_baseline / --impl reference) -------
+
+// Full single-thread reference pipeline: compute_order + effective_adjacency
+// + count_node_iterator_n.  Returns seconds; *total = T.
+double ref_time_sequential(void* h, uint64_t* total) {
+  auto* r = static_cast<RefGraph*>(h);
+  double t0 = now_s();
+  auto ord = compute_order(r->g, OrderKind::by_degree());
+  auto eff = effective_adjacency(r->g, ord);
+  *total = count_node_iterator_n(eff);
+  return now_s() - t0;
+}
+
+// Precomputes order + effective adjacency (untimed setup for the AOP sample).
+void ref_prepare(void* h) { static_cast<RefGraph*>(h)->effective(); }
+
+// Reference AOP rank bodies on host threads: the DPD prefix-sum plan for
+// `parts` ranks (partition.hpp:116-141), then for each rank id in `which`
+// build_overlap_partition (partition.hpp:171-206) + aop_count
+// (engines.hpp:38-54) on a pool of `threads` std::threads.  Reports the
+// oriented edges (sum of effdeg over the sampled cores), triangles, and the
+// wall time of the parallel region.
+double ref_aop_sample(void* h, uint64_t parts, const uint64_t* which, uint64_t nwhich,
+                      int threads, uint64_t* edges, uint64_t* tris) {
+  auto* r = static_cast<RefGraph*>(h);
+  const auto& eff = r->effective();
+  auto costs = node_costs(r->g, eff, CostKind::Dpd);
+  auto plan = compute_boundaries(costs, parts);
+  std::atomic<uint64_t> next{0}, e_acc{0}, t_acc{0};
+  double t0 = now_s();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&] {
+      for (;;) {
+        uint64_t k = next.fetch_add(1);
+        if (k >= nwhich) break;
+        uint64_t i = which[k];
+        auto part = build_overlap_partition(r->g, eff, plan, i);
+        NullSink sink;
+        uint64_t tt = aop_count(part, sink);
+        uint64_t ee = 0;
+        for (NodeId v = part.core_begin; v < part.core_end; ++v) ee += eff.effdeg(v);
+        e_acc += ee;
+        t_acc += tt;
+      }
+    });
+  for (auto& th : pool) th.join();
+  double dt = now_s() - t0;
+  *edges = e_acc.load();
+  *tris = t_acc.load();
+  return dt;
+}
+
+}  // extern "C"
