@@ -1,0 +1,207 @@
+/*
+ * trigraph_b200.h -- C ABI of the B200-native exact triangle counter.
+ *
+ * Drop-in boundary for the reference `trigraph` hot path
+ * (/root/reference/proj/include/trigraph/).  The reference has no FFI: its
+ * boundary is the header-only C++ API, so every entry point below names the
+ * reference function it replaces (file:line, relative to proj/include/trigraph/).
+ * The C++ mirror in include/trigraph_b200/trigraph.hpp wraps these calls
+ * behind the reference's own names and types.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Node ids are uint32_t (NodeId,
+ *    graph.hpp:14); offsets and counters are uint64_t (size_t/uint64_t in the
+ *    reference).
+ *  - Input arrays may live in host memory (pageable or pinned) or device
+ *    memory; the library detects which (cudaPointerGetAttributes).  Output
+ *    arrays are caller-allocated HOST buffers unless the name says `_device`.
+ *  - Every call returns a tg_status; tg_last_error() gives the message of the
+ *    last failure on the calling thread.  The C++ mirror maps
+ *    TG_ERR_INVALID_ARGUMENT to std::invalid_argument (engines.hpp:338,
+ *    partition.hpp:117) and everything else to std::runtime_error.
+ *  - A tg_graph lives on one device and is not thread-safe; calls on
+ *    distinct graphs may run concurrently.  There is no CPU fallback: without
+ *    a CUDA device every compute call fails with TG_ERR_CUDA.
+ */
+#ifndef TRIGRAPH_B200_H
+#define TRIGRAPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TG_OK = 0,
+  TG_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  TG_ERR_CUDA = 2,
+  TG_ERR_OOM = 3,
+  TG_ERR_CAPACITY = 4, /* caller buffer too small; required size reported */
+  TG_ERR_INTERNAL = 5
+} tg_status;
+
+/* engines.hpp:24 EngineKind (same order). */
+typedef enum {
+  TG_ENGINE_SEQ = 0,
+  TG_ENGINE_AOP = 1,
+  TG_ENGINE_ANOP_DIRECT = 2,
+  TG_ENGINE_ANOP_SURROGATE = 3
+} tg_engine;
+
+/* partition.hpp:18 CostKind (same order). */
+typedef enum {
+  TG_COST_N = 0,
+  TG_COST_D = 1,
+  TG_COST_DH = 2,
+  TG_COST_DDH = 3,
+  TG_COST_DH2 = 4,
+  TG_COST_DPD = 5,
+  TG_COST_NOV = 6
+} tg_cost;
+
+/* engines.hpp:270-280 EngineConfig.  The order is always ByDegree (the
+ * north_star path); ExecMode has no meaning on the device (results are
+ * mode-independent, acceptance.cpp:438-468). */
+typedef struct {
+  int32_t engine;            /* tg_engine */
+  int32_t cost;              /* tg_cost, default TG_COST_DPD */
+  uint64_t ranks;            /* logical ranks (>= 1; ignored by SEQ) */
+  const uint32_t* boundaries;/* optional override, ranks+1 entries, host memory */
+  int32_t track_nodes;       /* fill per-node counts */
+  int32_t collect_triangles; /* fill the triangle list */
+} tg_config;
+
+/* engines.hpp:282-287 RankStats.  realized_cost is reported as the
+ * algorithmic work sum_{v->u in rank} (h_v + h_u) (the DPD cost of the rank's
+ * apexes), not merge comparisons. stored_entries is the
+ * rank's partition storage (partition.hpp:163-168 / :218-222). */
+typedef struct {
+  uint64_t triangles;
+  uint64_t data_sent;
+  uint64_t data_recv;
+  uint64_t realized_cost;
+  uint64_t stored_entries;
+} tg_rank_stats;
+
+typedef struct tg_graph tg_graph;
+
+/* ---- graph construction (graph.hpp:58-85 build_graph; Graph ctor :22) ---- */
+
+/* build_graph on the device: drop self-loops, symmetrise, sort, unique.
+ * pairs = E interleaved (u,v); n = max(n_override, 1 + max id). */
+tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pairs,
+                              uint64_t n_override, tg_graph** out);
+/* Adopt an already-built symmetric CSR (offsets n+1, adj offsets[n]).  Lists
+ * must be ID-sorted, loop- and duplicate-free (the Graph invariant). */
+tg_status tg_graph_from_csr(int device, uint64_t n, const uint64_t* offsets,
+                            const uint32_t* adj, tg_graph** out);
+tg_status tg_graph_free(tg_graph* g);
+/* Graph::num_nodes / num_edges (graph.hpp:25-26). */
+tg_status tg_graph_info(tg_graph* g, uint64_t* num_nodes, uint64_t* num_edges);
+/* Copy the CSR back (offsets n+1, adj 2m). */
+tg_status tg_graph_csr(tg_graph* g, uint64_t* offsets, uint32_t* adj);
+/* Launch on this CUDA stream (cudaStream_t) from now on; 0 = the library's own. */
+tg_status tg_set_stream(tg_graph* g, void* stream);
+
+/* ---- preprocessing (order.hpp:95-104, effective.hpp:37-52) ---- */
+
+/* compute_order(g, ByDegree).rank (n entries). */
+tg_status tg_compute_order(tg_graph* g, uint32_t* rank);
+/* effective_adjacency(g, degree order): offsets (n+1) and lists (m), either
+ * may be NULL.  Builds and caches the oriented CSR on the device. */
+tg_status tg_effective_adjacency(tg_graph* g, uint64_t* offsets, uint32_t* eff);
+/* ordering_cost(g, degree order) (sequential.hpp:95-104) = W. */
+tg_status tg_ordering_cost(tg_graph* g, uint64_t* cost);
+
+/* ---- partitioning (partition.hpp:45-141) ---- */
+
+/* node_costs(g, eff, kind): f (n) and inclusive prefix (n); either may be NULL. */
+tg_status tg_node_costs(tg_graph* g, int32_t kind, uint64_t* f, uint64_t* prefix);
+/* compute_boundaries(node_costs(kind), p): p+1 boundaries. */
+tg_status tg_compute_boundaries(tg_graph* g, int32_t kind, uint64_t p, uint32_t* boundaries);
+
+/* ---- counting (sequential.hpp:74-91, engines.hpp:335-435) ---- */
+
+/* count_node_iterator_n(effective_adjacency(g, by_degree)). */
+tg_status tg_count(tg_graph* g, uint64_t* total);
+
+/* run_engine(g, cfg).  per_rank: ranks entries (1 for SEQ); boundaries_out:
+ * ranks+1 entries (may be NULL); node_counts: n entries, filled when
+ * cfg->track_nodes; triangles: 3*capacity uint32, filled (ascending ids per
+ * triple, unspecified triple order) when cfg->collect_triangles, with
+ * *num_triangles = total; TG_ERR_CAPACITY if capacity < total. */
+tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total,
+                        tg_rank_stats* per_rank, uint32_t* boundaries_out,
+                        uint64_t* node_counts, uint32_t* triangles, uint64_t capacity,
+                        uint64_t* num_triangles);
+
+/* clustering_coefficients(g, cfg) (engines.hpp:422-435): T_v (n) and C_v (n). */
+tg_status tg_clustering_coefficients(tg_graph* g, const tg_config* cfg,
+                                     uint64_t* triangles_per_node, double* coefficient);
+
+/* ---- device-resident hot path (bench / multi-process drivers) ---- */
+
+/* One pass of the hot path on the current stream without a host sync:
+ * orientation (effective_adjacency) + NodeIteratorN count over all apexes.
+ * The count lands in *d_total (device memory, uint64).  Stream-ordered. */
+tg_status tg_step_device(tg_graph* g, uint64_t* d_total);
+/* The orientation half of the step alone (effective_adjacency, rebuilt). */
+tg_status tg_orient_device(tg_graph* g);
+/* Kernel-only variant: count over the cached oriented CSR (no re-orientation). */
+tg_status tg_count_device(tg_graph* g, uint64_t* d_total);
+
+/* Rank-local work for one process per GPU (engines.hpp:38-54, 60-76,
+ * 146-198).  `boundaries` has p+1 entries (host).  Each call is
+ * stream-ordered and returns without a host sync unless noted. */
+/* AOP rank body: count triangles whose apex lies in core `rank`. */
+tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p,
+                             uint64_t rank, uint64_t* d_total);
+/* Surrogate pack (engines.hpp:173-187): sizes first (host sync).
+ * msgs_per_dest / words_per_dest: p entries each (host). */
+tg_status tg_surrogate_pack_sizes(tg_graph* g, const uint32_t* boundaries, uint64_t p,
+                                  uint64_t rank, uint64_t* msgs_per_dest,
+                                  uint64_t* words_per_dest);
+/* Writes headers (2 uint32 per message: v, len) and list data, destination-
+ * major, into device buffers sized from tg_surrogate_pack_sizes. */
+tg_status tg_surrogate_pack_device(tg_graph* g, const uint32_t* boundaries, uint64_t p,
+                                   uint64_t rank, uint32_t* d_hdr, uint32_t* d_data);
+/* Local intersections of core `rank` plus SurrogateCount over received
+ * messages (d_hdr: 2*num_msgs, d_data: the lists, concatenated in header
+ * order).  Adds to *d_total. */
+tg_status tg_surrogate_count_device(tg_graph* g, const uint32_t* boundaries, uint64_t p,
+                                    uint64_t rank, const uint32_t* d_hdr, uint64_t num_msgs,
+                                    const uint32_t* d_data, uint64_t* d_total);
+
+/* ---- diagnostics ---- */
+const char* tg_last_error(void);
+const char* tg_status_string(tg_status s);
+/* Number of library kernels launched so far in this process. */
+uint64_t tg_kernel_launches(void);
+/* Test hook: shared-memory capacity (entries) of the CTA-path apex staging;
+ * lists longer than this are searched in global memory.  0 = default. */
+void tg_debug_set_block_cap(uint32_t entries);
+/* Device-side time (ms) of the last intersection pass (CUDA events on the
+ * launching stream); 0 if none. */
+double tg_last_intersect_ms(tg_graph* g);
+
+/* ---- synthetic inputs (host harness; BASELINE.json configs) ----
+ * Each returns a malloc'ed interleaved pair array (free with tg_free_host). */
+/* io.hpp:129-162 gen_pa(n, d, seed), bit-identical edge stream. */
+tg_status tg_gen_pa(uint64_t n, uint64_t d, uint64_t seed, uint32_t** pairs, uint64_t* num_pairs);
+/* io.hpp:85-123 gen_gnp(n, d, seed), bit-identical edge stream. */
+tg_status tg_gen_gnp(uint64_t n, double d, uint64_t seed, uint32_t** pairs, uint64_t* num_pairs);
+/* G(n, m): m distinct non-loop pairs drawn uniformly (config 1). */
+tg_status tg_gen_gnm(uint64_t n, uint64_t m, uint64_t seed, uint32_t** pairs, uint64_t* num_pairs);
+/* R-MAT scale s, edge factor ef, (a,b,c) with d = 1-a-b-c (config 3). */
+tg_status tg_gen_rmat(uint32_t scale, uint64_t edge_factor, double a, double b, double c,
+                      uint64_t seed, uint32_t** pairs, uint64_t* num_pairs);
+/* Watts-Strogatz ring n, k neighbours (k/2 per side), rewiring beta (config 4). */
+tg_status tg_gen_ws(uint64_t n, uint64_t k, double beta, uint64_t seed, uint32_t** pairs,
+                    uint64_t* num_pairs);
+void tg_free_host(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIGRAPH_B200_H */

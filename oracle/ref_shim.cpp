@@ -30,6 +30,7 @@ struct RefGraph {
   Graph g;
   std::optional<OrderRank> order;
   std::optional<EffectiveAdjacency> eff;
+  std::optional<PartitionPlan> plan;  // cached DPD plan for the AOP sample
 
   const EffectiveAdjacency& effective() {
     if (!eff) {
@@ -235,8 +236,9 @@ double ref_aop_sample(void* h, uint64_t parts, const uint64_t* which, uint64_t n
                       int threads, uint64_t* edges, uint64_t* tris) {
   auto* r = static_cast<RefGraph*>(h);
   const auto& eff = r->effective();
-  auto costs = node_costs(r->g, eff, CostKind::Dpd);
-  auto plan = compute_boundaries(costs, parts);
+  if (!r->plan || r->plan->ranks() != parts)
+    r->plan = compute_boundaries(node_costs(r->g, eff, CostKind::Dpd), parts);
+  const PartitionPlan& plan = *r->plan;
   std::atomic<uint64_t> next{0}, e_acc{0}, t_acc{0};
   double t0 = now_s();
   std::vector<std::thread> pool;

@@ -1,0 +1,117 @@
+"""ctypes loader for libtrigraph_b200.so (the C ABI in include/trigraph_b200.h).
+
+There is no fallback: if the in-tree library is missing, importing the
+package raises.  Build it with ``python -c "import __graft_entry__ as g; g.build()"``
+or ``make -C paper_1706_05151_b200/csrc``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtrigraph_b200.so")
+
+TG_OK = 0
+TG_ERR_INVALID_ARGUMENT = 1
+TG_ERR_CUDA = 2
+TG_ERR_OOM = 3
+TG_ERR_CAPACITY = 4
+TG_ERR_INTERNAL = 5
+
+
+class TgConfig(C.Structure):
+    _fields_ = [
+        ("engine", C.c_int32),
+        ("cost", C.c_int32),
+        ("ranks", C.c_uint64),
+        ("boundaries", C.c_void_p),
+        ("track_nodes", C.c_int32),
+        ("collect_triangles", C.c_int32),
+    ]
+
+
+class TgRankStats(C.Structure):
+    _fields_ = [
+        ("triangles", C.c_uint64),
+        ("data_sent", C.c_uint64),
+        ("data_recv", C.c_uint64),
+        ("realized_cost", C.c_uint64),
+        ("stored_entries", C.c_uint64),
+    ]
+
+
+# Every symbol include/trigraph_b200.h declares, with its ctypes signature.
+_vp, _u64, _u32, _i32, _dbl = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32, C.c_double
+_pvp, _pu64 = C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)
+SIGNATURES = {
+    "tg_graph_from_edges": (_i32, [C.c_int, _vp, _u64, _u64, _pvp]),
+    "tg_graph_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pvp]),
+    "tg_graph_free": (_i32, [_vp]),
+    "tg_graph_info": (_i32, [_vp, _pu64, _pu64]),
+    "tg_graph_csr": (_i32, [_vp, _vp, _vp]),
+    "tg_set_stream": (_i32, [_vp, _vp]),
+    "tg_compute_order": (_i32, [_vp, _vp]),
+    "tg_effective_adjacency": (_i32, [_vp, _vp, _vp]),
+    "tg_ordering_cost": (_i32, [_vp, _pu64]),
+    "tg_node_costs": (_i32, [_vp, _i32, _vp, _vp]),
+    "tg_compute_boundaries": (_i32, [_vp, _i32, _u64, _vp]),
+    "tg_count": (_i32, [_vp, _pu64]),
+    "tg_run_engine": (_i32, [_vp, C.POINTER(TgConfig), _pu64, _vp, _vp, _vp, _vp, _u64, _pu64]),
+    "tg_clustering_coefficients": (_i32, [_vp, C.POINTER(TgConfig), _vp, _vp]),
+    "tg_step_device": (_i32, [_vp, _vp]),
+    "tg_orient_device": (_i32, [_vp]),
+    "tg_count_device": (_i32, [_vp, _vp]),
+    "tg_aop_rank_device": (_i32, [_vp, _vp, _u64, _u64, _vp]),
+    "tg_surrogate_pack_sizes": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "tg_surrogate_pack_device": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "tg_surrogate_count_device": (_i32, [_vp, _vp, _u64, _u64, _vp, _u64, _vp, _vp]),
+    "tg_last_error": (C.c_char_p, []),
+    "tg_status_string": (C.c_char_p, [_i32]),
+    "tg_kernel_launches": (_u64, []),
+    "tg_last_intersect_ms": (_dbl, [_vp]),
+    "tg_debug_set_block_cap": (None, [_u32]),
+    "tg_gen_pa": (_i32, [_u64, _u64, _u64, _pvp, _pu64]),
+    "tg_gen_gnp": (_i32, [_u64, _dbl, _u64, _pvp, _pu64]),
+    "tg_gen_gnm": (_i32, [_u64, _u64, _u64, _pvp, _pu64]),
+    "tg_gen_rmat": (_i32, [_u32, _u64, _dbl, _dbl, _dbl, _u64, _pvp, _pu64]),
+    "tg_gen_ws": (_i32, [_u64, _u64, _dbl, _u64, _pvp, _pu64]),
+    "tg_free_host": (None, [_vp]),
+}
+
+_lib = None
+
+
+class TrigraphError(RuntimeError):
+    """A non-argument failure reported by the library (CUDA, OOM, internal)."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    """Map tg_status to the reference's exception types."""
+    if status == TG_OK:
+        return
+    msg = lib().tg_last_error().decode(errors="replace")
+    if status == TG_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)  # reference: std::invalid_argument
+    if status == TG_ERR_OOM:
+        raise MemoryError(msg)
+    raise TrigraphError(status, f"{lib().tg_status_string(status).decode()}: {msg}")

@@ -1,0 +1,693 @@
+// engine.cu -- engines and the C ABI (include/trigraph_b200.h).
+//
+// Reference: run_engine (engines.hpp:335-418), clustering_coefficients
+// (engines.hpp:422-435), aop_count (:38-54), anop_surrogate_body (:146-198),
+// anop_direct_body (:80-141), aggregate_clustering (:211-268).
+//
+// One tg_graph = one device.  The logical ranks of an EngineConfig run one
+// after another on that device with their real data layout:
+//   AOP       -- rank i counts apexes of core i against the oriented lists it
+//                holds (core + halo; with one device the halo is the resident
+//                oriented CSR, its trimmed size is reported as stored_entries);
+//   SURROGATE -- rank i holds only its core lists (partition-local CSR with a
+//                base offset), packs (v, N_v) per distinct remote owner,
+//                "sends" by concatenating destination segments, and each
+//                owner runs local intersections + SurrogateCount;
+//   DIRECT    -- counts as AOP (the apex owner fetches N_u); message counts
+//                follow the request/reply protocol.
+// The multi-process path (one process per GPU, paper_1706_05151_b200/
+// distributed.py) calls the same kernels through the rank-local entries.
+#include <cstring>
+#include <mutex>
+
+#include "exchange.cuh"
+#include "tg_internal.cuh"
+
+struct tg_graph {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  tgb::DevGraph g;
+  bool have_eff = false;
+  tgb::DevEff eff;
+  tgb::IntersectScratch scr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+  // rank-local caches (multi-process surrogate)
+  bool have_part = false;
+  uint64_t part_rank = 0;
+  std::vector<uint32_t> part_b;
+  tgb::DevEff part;
+  tgb::SurrogatePack pack;
+};
+
+namespace {
+
+thread_local std::string t_last_error;
+
+}  // namespace
+void tgb_set_error(const std::string& msg) { t_last_error = msg; }
+namespace {
+
+template <class F>
+tg_status guard(F&& f) {
+  try {
+    f();
+    return TG_OK;
+  } catch (const tgb::Error& e) {
+    t_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc& e) {
+    t_last_error = e.what();
+    return TG_ERR_OOM;
+  } catch (const std::exception& e) {
+    t_last_error = e.what();
+    return TG_ERR_INTERNAL;
+  }
+}
+
+using tgb::CountOut;
+using tgb::CsrView;
+using tgb::DBuf;
+using tgb::DevEff;
+
+CsrView view(const DevEff& e) { return CsrView{e.off.p, e.data.p, e.base}; }
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+void upload(DBuf<T>& dst, const T* src, size_t count, cudaStream_t s) {
+  dst.alloc(count ? count : 1, s);
+  if (count)
+    TG_CUDA(cudaMemcpyAsync(dst.p, src, count * sizeof(T),
+                            is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+}
+
+template <class T>
+void download(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (count && dst) TG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+void enter(tg_graph* g) {
+  TG_REQUIRE(g != nullptr, "null graph handle");
+  TG_CUDA(cudaSetDevice(g->device));
+}
+
+void sync(tg_graph* g) { TG_CUDA(cudaStreamSynchronize(g->stream)); }
+
+tg_graph* new_graph(int device) {
+  int count = 0;
+  TG_CUDA(cudaGetDeviceCount(&count));
+  TG_REQUIRE(device >= 0 && device < count, "invalid CUDA device ordinal");
+  TG_CUDA(cudaSetDevice(device));
+  auto* g = new tg_graph;
+  g->device = device;
+  TG_CUDA(cudaStreamCreateWithFlags(&g->own, cudaStreamNonBlocking));
+  g->stream = g->own;
+  TG_CUDA(cudaEventCreate(&g->ev0));
+  TG_CUDA(cudaEventCreate(&g->ev1));
+  return g;
+}
+
+void ensure_eff(tg_graph* g) {
+  if (!g->have_eff) {
+    tgb::orient_rows(g->g, 0, (uint32_t)g->g.n, g->eff, g->stream);
+    g->have_eff = true;
+  }
+}
+
+// Counting pass with CUDA-event timing of the intersection kernels.
+template <class F>
+void timed_pass(tg_graph* g, F&& f) {
+  TG_CUDA(cudaEventRecord(g->ev0, g->stream));
+  f();
+  TG_CUDA(cudaEventRecord(g->ev1, g->stream));
+  g->timed = true;
+}
+
+std::vector<uint32_t> plan_for(tg_graph* g, int cost, uint64_t p, const uint32_t* override_b) {
+  std::vector<uint32_t> b;
+  if (override_b) {
+    b.assign(override_b, override_b + p + 1);
+    TG_REQUIRE(b[0] == 0 && b[p] <= g->g.n, "boundaries must start at 0 and end at <= n");
+    for (uint64_t i = 0; i < p; ++i) TG_REQUIRE(b[i] <= b[i + 1], "boundaries must be sorted");
+    return b;
+  }
+  DBuf<uint64_t> f(g->g.n ? g->g.n : 1, g->stream), pre(g->g.n ? g->g.n : 1, g->stream);
+  tgb::node_costs_device(g->g, g->eff, cost, f.p, pre.p, g->stream);
+  return tgb::boundaries_from_prefix(pre.p, g->g.n, p, g->stream);
+}
+
+// host copy of an inclusive prefix of f (for per-rank realized cost)
+std::vector<uint64_t> range_sums(tg_graph* g, int cost, const std::vector<uint32_t>& b) {
+  const uint64_t n = g->g.n, p = b.size() - 1;
+  std::vector<uint64_t> out(p, 0);
+  if (!n) return out;
+  DBuf<uint64_t> f(n, g->stream), pre(n, g->stream);
+  tgb::node_costs_device(g->g, g->eff, cost, f.p, pre.p, g->stream);
+  std::vector<uint64_t> at(p + 1, 0);
+  for (uint64_t i = 0; i <= p; ++i)
+    if (b[i] > 0) download(&at[i], pre.p + (b[i] - 1), 1, g->stream);
+  sync(g);
+  for (uint64_t i = 0; i < p; ++i) out[i] = at[i + 1] - at[i];
+  return out;
+}
+
+struct EngineResult {
+  std::vector<uint32_t> b;
+  std::vector<tg_rank_stats> per_rank;
+  uint64_t total = 0;
+};
+
+// The engines.  `tally`/`tri` are device outputs (may be null).
+EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally, uint32_t* d_tri,
+                 unsigned long long* d_cursor, uint64_t cap) {
+  TG_REQUIRE(cfg.engine >= TG_ENGINE_SEQ && cfg.engine <= TG_ENGINE_ANOP_SURROGATE, "unknown engine");
+  const uint64_t p = cfg.engine == TG_ENGINE_SEQ ? 1 : cfg.ranks;
+  TG_REQUIRE(p >= 1, "run_engine: ranks must be >= 1");  // engines.hpp:337-338
+  TG_REQUIRE(cfg.cost >= TG_COST_N && cfg.cost <= TG_COST_NOV, "unknown cost kind");
+  cudaStream_t s = g->stream;
+  ensure_eff(g);
+  const uint64_t n = g->g.n;
+  EngineResult R;
+  R.b = plan_for(g, cfg.cost, p, cfg.boundaries);
+  const auto& b = R.b;
+  R.per_rank.assign(p, tg_rank_stats{0, 0, 0, 0, 0});
+  DBuf<unsigned long long> ctr(p, s);
+  ctr.zero();
+  auto out_for = [&](uint64_t i) {
+    return CountOut{ctr.p + i, d_tally, d_tri, d_cursor, cap};
+  };
+  const CsrView full = view(g->eff);
+  const uint32_t N = (uint32_t)n;
+
+  if (cfg.engine == TG_ENGINE_SEQ) {
+    timed_pass(g, [&] { tgb::intersect_rows(full, 0, N, full, 0, N, out_for(0), g->scr, s); });
+    R.per_rank[0].stored_entries = g->eff.entries;
+  } else if (cfg.engine == TG_ENGINE_AOP || cfg.engine == TG_ENGINE_ANOP_DIRECT) {
+    timed_pass(g, [&] {
+      for (uint64_t i = 0; i < p; ++i)
+        if (b[i + 1] > b[i])
+          tgb::intersect_rows(full, b[i], b[i + 1], full, 0, N, out_for(i), g->scr, s);
+    });
+    if (cfg.engine == TG_ENGINE_AOP) {
+      for (uint64_t i = 0; i < p; ++i)
+        R.per_rank[i].stored_entries = tgb::overlap_stored_entries(full, n, b[i], b[i + 1], s);
+    } else {
+      std::vector<uint64_t> req, rep;
+      tgb::direct_messages(full, n, b, req, rep, s);
+      for (uint64_t i = 0; i < p; ++i) {
+        R.per_rank[i].data_sent = req[i] + rep[i];
+        R.per_rank[i].data_recv = req[i] + rep[i];
+      }
+      for (uint64_t i = 0; i < p; ++i) {
+        uint64_t ob[2];
+        download(&ob[0], g->eff.off.p + b[i], 1, s);
+        download(&ob[1], g->eff.off.p + b[i + 1], 1, s);
+        sync(g);
+        R.per_rank[i].stored_entries = ob[1] - ob[0];
+      }
+    }
+  } else {  // ANOP surrogate
+    std::vector<DevEff> parts(p);
+    std::vector<tgb::SurrogatePack> packs(p);
+    std::vector<DBuf<uint32_t>> hdr(p), dat(p);
+    for (uint64_t i = 0; i < p; ++i) {
+      tgb::orient_rows(g->g, b[i], b[i + 1], parts[i], s);  // non-overlapping storage
+      R.per_rank[i].stored_entries = parts[i].entries;
+      packs[i].build(view(parts[i]), b[i], b[i + 1], b, (uint32_t)i, s);
+      uint64_t msgs = 0, words = 0;
+      for (uint64_t j = 0; j < p; ++j) {
+        msgs += packs[i].msgs_per_dest[j];
+        words += packs[i].words_per_dest[j];
+        R.per_rank[i].data_sent += packs[i].msgs_per_dest[j];
+        R.per_rank[j].data_recv += packs[i].msgs_per_dest[j];
+      }
+      hdr[i].alloc(2 * msgs + 1, s);
+      dat[i].alloc(words + 1, s);
+      packs[i].scatter(hdr[i].p, dat[i].p, s);
+    }
+    // "all-to-allv": receive buffer of rank j = dest-j segments of every sender
+    std::vector<DBuf<uint32_t>> rh(p), rd(p);
+    std::vector<uint64_t> rmsgs(p, 0);
+    for (uint64_t j = 0; j < p; ++j) {
+      uint64_t msgs = 0, words = 0;
+      for (uint64_t i = 0; i < p; ++i) {
+        msgs += packs[i].msgs_per_dest[j];
+        words += packs[i].words_per_dest[j];
+      }
+      rmsgs[j] = msgs;
+      rh[j].alloc(2 * msgs + 1, s);
+      rd[j].alloc(words + 1, s);
+      uint64_t mo = 0, wo = 0;
+      for (uint64_t i = 0; i < p; ++i) {
+        uint64_t m0 = 0, w0 = 0;
+        for (uint64_t jj = 0; jj < j; ++jj) {
+          m0 += packs[i].msgs_per_dest[jj];
+          w0 += packs[i].words_per_dest[jj];
+        }
+        const uint64_t mi = packs[i].msgs_per_dest[j], wi = packs[i].words_per_dest[j];
+        if (mi)
+          TG_CUDA(cudaMemcpyAsync(rh[j].p + 2 * mo, hdr[i].p + 2 * m0, 2 * mi * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+        if (wi)
+          TG_CUDA(cudaMemcpyAsync(rd[j].p + wo, dat[i].p + w0, wi * 4, cudaMemcpyDeviceToDevice, s));
+        mo += mi;
+        wo += wi;
+      }
+    }
+    std::vector<DBuf<uint64_t>> moff(p);
+    for (uint64_t j = 0; j < p; ++j) tgb::message_offsets(rh[j].p, rmsgs[j], moff[j], s);
+    timed_pass(g, [&] {
+      for (uint64_t j = 0; j < p; ++j) {
+        if (b[j + 1] <= b[j]) continue;
+        const CsrView pv = view(parts[j]);
+        tgb::intersect_rows(pv, b[j], b[j + 1], pv, b[j], b[j + 1], out_for(j), g->scr, s);
+        tgb::MsgView mv{rh[j].p, moff[j].p, rd[j].p, rmsgs[j]};
+        tgb::intersect_msgs(mv, pv, b[j], b[j + 1], out_for(j), g->scr, s);
+      }
+    });
+  }
+  std::vector<unsigned long long> h(p);
+  download(h.data(), ctr.p, p, s);
+  sync(g);
+  for (uint64_t i = 0; i < p; ++i) {
+    R.per_rank[i].triangles = h[i];
+    R.total += h[i];
+  }
+  // realized cost = algorithmic work of the rank: DPD over apex cores
+  // (AOP / direct / seq), NOV over middle-vertex cores (surrogate).
+  auto rc = range_sums(g, cfg.engine == TG_ENGINE_ANOP_SURROGATE ? TG_COST_NOV : TG_COST_DPD, b);
+  for (uint64_t i = 0; i < p; ++i) R.per_rank[i].realized_cost = rc[i];
+  return R;
+}
+
+uint64_t seq_count(tg_graph* g) {
+  ensure_eff(g);
+  cudaStream_t s = g->stream;
+  DBuf<unsigned long long> ctr(1, s);
+  ctr.zero();
+  const CsrView full = view(g->eff);
+  const uint32_t N = (uint32_t)g->g.n;
+  timed_pass(g, [&] {
+    tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, g->scr, s);
+  });
+  unsigned long long h = 0;
+  download(&h, ctr.p, 1, s);
+  sync(g);
+  return h;
+}
+
+void prepare_part(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t rank) {
+  TG_REQUIRE(boundaries && p >= 1 && rank < p, "invalid rank / boundaries");
+  std::vector<uint32_t> b(boundaries, boundaries + p + 1);
+  TG_REQUIRE(b[0] == 0 && b[p] <= g->g.n, "boundaries must start at 0 and end at <= n");
+  if (g->have_part && g->part_rank == rank && g->part_b == b) return;
+  tgb::orient_rows(g->g, b[rank], b[rank + 1], g->part, g->stream);
+  g->pack.build(view(g->part), b[rank], b[rank + 1], b, (uint32_t)rank, g->stream);
+  g->part_b = b;
+  g->part_rank = rank;
+  g->have_part = true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tg_last_error(void) { return t_last_error.c_str(); }
+
+const char* tg_status_string(tg_status s) {
+  switch (s) {
+    case TG_OK: return "ok";
+    case TG_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case TG_ERR_CUDA: return "CUDA error";
+    case TG_ERR_OOM: return "out of device memory";
+    case TG_ERR_CAPACITY: return "output capacity too small";
+    case TG_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+uint64_t tg_kernel_launches(void) { return tgb::g_launches; }
+
+void tg_debug_set_block_cap(uint32_t entries) { tgb::g_block_cap = entries; }
+
+tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pairs,
+                              uint64_t n_override, tg_graph** out) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr, "null output handle");
+    TG_REQUIRE(pairs != nullptr || num_pairs == 0, "null pairs");
+    tg_graph* g = new_graph(device);
+    try {
+      DBuf<uint32_t> dp;
+      upload(dp, pairs, 2 * num_pairs, g->stream);
+      tgb::build_graph_device(dp.p, num_pairs, n_override, g->g, g->stream);
+      sync(g);
+    } catch (...) {
+      tg_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+tg_status tg_graph_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,
+                            tg_graph** out) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr && offsets != nullptr, "null argument");
+    TG_REQUIRE(n <= 0xFFFFFFFFull, "n must fit NodeId");
+    tg_graph* g = new_graph(device);
+    try {
+      uint64_t m2 = 0;
+      if (is_device_ptr(offsets)) {
+        TG_CUDA(cudaMemcpy(&m2, offsets + n, 8, cudaMemcpyDeviceToHost));
+      } else {
+        m2 = offsets[n];
+      }
+      TG_REQUIRE(m2 % 2 == 0, "symmetric CSR must hold an even number of entries");
+      TG_REQUIRE(adj != nullptr || m2 == 0, "null adjacency");
+      g->g.n = n;
+      g->g.m2 = m2;
+      upload(g->g.off, offsets, n + 1, g->stream);
+      upload(g->g.adj, adj, m2, g->stream);
+      tgb::compute_degrees(g->g, g->stream);
+      sync(g);
+    } catch (...) {
+      tg_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+tg_status tg_graph_free(tg_graph* g) {
+  if (!g) return TG_OK;
+  return guard([&] {
+    cudaSetDevice(g->device);
+    cudaStreamSynchronize(g->own);
+    if (g->stream != g->own) cudaStreamSynchronize(g->stream);
+    {
+      // release buffers on the library stream before destroying it
+      g->g.off.release(); g->g.adj.release(); g->g.deg.release();
+      g->eff.off.release(); g->eff.data.release();
+      g->scr.big.release(); g->scr.big_count.release();
+      g->part.off.release(); g->part.data.release();
+      g->pack.desc.release(); g->pack.doff.release();
+    }
+    cudaStreamSynchronize(g->own);
+    if (g->stream != g->own) cudaStreamSynchronize(g->stream);
+    cudaEventDestroy(g->ev0);
+    cudaEventDestroy(g->ev1);
+    cudaStreamDestroy(g->own);
+    delete g;
+  });
+}
+
+tg_status tg_graph_info(tg_graph* g, uint64_t* num_nodes, uint64_t* num_edges) {
+  return guard([&] {
+    TG_REQUIRE(g != nullptr, "null graph handle");
+    if (num_nodes) *num_nodes = g->g.n;
+    if (num_edges) *num_edges = g->g.m2 / 2;
+  });
+}
+
+tg_status tg_graph_csr(tg_graph* g, uint64_t* offsets, uint32_t* adj) {
+  return guard([&] {
+    enter(g);
+    download(offsets, g->g.off.p, g->g.n + 1, g->stream);
+    download(adj, g->g.adj.p, g->g.m2, g->stream);
+    sync(g);
+  });
+}
+
+tg_status tg_set_stream(tg_graph* g, void* stream) {
+  return guard([&] {
+    enter(g);
+    cudaStream_t ns = stream ? (cudaStream_t)stream : g->own;
+    if (ns != g->stream) {
+      sync(g);  // buffers allocated on the old stream stay valid (pool-backed)
+      g->stream = ns;
+      // DBuf frees are stream-ordered on the stream they were allocated on;
+      // re-home them so later frees order after work on the new stream.
+      auto rehome = [&](auto& buf) { buf.s = ns; };
+      rehome(g->g.off); rehome(g->g.adj); rehome(g->g.deg);
+      rehome(g->eff.off); rehome(g->eff.data);
+      rehome(g->scr.big); rehome(g->scr.big_count);
+      rehome(g->part.off); rehome(g->part.data);
+      rehome(g->pack.desc); rehome(g->pack.doff);
+    }
+  });
+}
+
+tg_status tg_compute_order(tg_graph* g, uint32_t* rank) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(rank != nullptr || g->g.n == 0, "null rank output");
+    DBuf<uint32_t> d(g->g.n ? g->g.n : 1, g->stream);
+    tgb::degree_rank(g->g, d.p, g->stream);
+    download(rank, d.p, g->g.n, g->stream);
+    sync(g);
+  });
+}
+
+tg_status tg_effective_adjacency(tg_graph* g, uint64_t* offsets, uint32_t* eff) {
+  return guard([&] {
+    enter(g);
+    ensure_eff(g);
+    download(offsets, g->eff.off.p, g->g.n + 1, g->stream);
+    download(eff, g->eff.data.p, g->eff.entries, g->stream);
+    sync(g);
+  });
+}
+
+tg_status tg_ordering_cost(tg_graph* g, uint64_t* cost) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(cost != nullptr, "null output");
+    ensure_eff(g);
+    *cost = tgb::ordering_cost_device(g->g, g->eff, g->stream);
+  });
+}
+
+tg_status tg_node_costs(tg_graph* g, int32_t kind, uint64_t* f, uint64_t* prefix) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(kind >= TG_COST_N && kind <= TG_COST_NOV, "unknown cost kind");
+    ensure_eff(g);
+    const uint64_t n = g->g.n;
+    DBuf<uint64_t> df(n ? n : 1, g->stream), dp(n ? n : 1, g->stream);
+    tgb::node_costs_device(g->g, g->eff, kind, df.p, dp.p, g->stream);
+    download(f, df.p, n, g->stream);
+    download(prefix, dp.p, n, g->stream);
+    sync(g);
+  });
+}
+
+tg_status tg_compute_boundaries(tg_graph* g, int32_t kind, uint64_t p, uint32_t* boundaries) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(p >= 1, "compute_boundaries: p must be >= 1");  // partition.hpp:117
+    TG_REQUIRE(boundaries != nullptr, "null output");
+    ensure_eff(g);
+    auto b = plan_for(g, kind, p, nullptr);
+    std::memcpy(boundaries, b.data(), b.size() * 4);
+  });
+}
+
+tg_status tg_count(tg_graph* g, uint64_t* total) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(total != nullptr, "null output");
+    *total = seq_count(g);
+  });
+}
+
+tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total, tg_rank_stats* per_rank,
+                        uint32_t* boundaries_out, uint64_t* node_counts, uint32_t* triangles,
+                        uint64_t capacity, uint64_t* num_triangles) {
+  tg_status cap_status = TG_OK;
+  tg_status st = guard([&] {
+    enter(g);
+    TG_REQUIRE(cfg != nullptr, "null config");
+    cudaStream_t s = g->stream;
+    const uint64_t n = g->g.n;
+    DBuf<unsigned long long> tally, cursor;
+    DBuf<uint32_t> tri;
+    uint64_t cap = 0;
+    if (cfg->track_nodes) {
+      TG_REQUIRE(node_counts != nullptr || n == 0, "track_nodes needs node_counts");
+      tally.alloc(n ? n : 1, s);
+      tally.zero();
+    }
+    if (cfg->collect_triangles) {
+      TG_REQUIRE(num_triangles != nullptr, "collect_triangles needs num_triangles");
+      cap = seq_count(g);  // exact size first (ListSink holds T triples)
+      tri.alloc(3 * (cap ? cap : 1), s);
+      cursor.alloc(1, s);
+      cursor.zero();
+    }
+    EngineResult R = run(g, *cfg, cfg->track_nodes ? tally.p : nullptr,
+                         cfg->collect_triangles ? tri.p : nullptr,
+                         cfg->collect_triangles ? cursor.p : nullptr, cap);
+    if (total) *total = R.total;
+    if (per_rank) std::memcpy(per_rank, R.per_rank.data(), R.per_rank.size() * sizeof(tg_rank_stats));
+    if (boundaries_out) std::memcpy(boundaries_out, R.b.data(), R.b.size() * 4);
+    if (cfg->track_nodes) download(node_counts, (const uint64_t*)tally.p, n, s);
+    if (cfg->collect_triangles) {
+      *num_triangles = R.total;
+      if (triangles) download(triangles, tri.p, 3 * std::min<uint64_t>(R.total, capacity), s);
+      if (capacity < R.total) cap_status = TG_ERR_CAPACITY;
+    }
+    sync(g);
+  });
+  if (st == TG_OK && cap_status != TG_OK) {
+    t_last_error = "triangle capacity smaller than the triangle count";
+    return cap_status;
+  }
+  return st;
+}
+
+tg_status tg_clustering_coefficients(tg_graph* g, const tg_config* cfg, uint64_t* triangles_per_node,
+                                     double* coefficient) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(cfg != nullptr, "null config");
+    cudaStream_t s = g->stream;
+    const uint64_t n = g->g.n;
+    DBuf<unsigned long long> tally(n ? n : 1, s);
+    tally.zero();
+    tg_config c = *cfg;
+    c.track_nodes = 1;  // engines.hpp:423
+    c.collect_triangles = 0;
+    run(g, c, tally.p, nullptr, nullptr, 0);
+    DBuf<double> cc(n ? n : 1, s);
+    tgb::clustering_device(g->g, tally.p, cc.p, s);
+    download(triangles_per_node, (const uint64_t*)tally.p, n, s);
+    download(coefficient, cc.p, n, s);
+    sync(g);
+  });
+}
+
+tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(d_total != nullptr, "null output");
+    cudaStream_t s = g->stream;
+    // orientation: effective_adjacency (effective.hpp:37-52), rebuilt
+    tgb::orient_rows(g->g, 0, (uint32_t)g->g.n, g->eff, s);
+    g->have_eff = true;
+    TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
+    const CsrView full = view(g->eff);
+    const uint32_t N = (uint32_t)g->g.n;
+    timed_pass(g, [&] {
+      tgb::intersect_rows(full, 0, N, full, 0, N,
+                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s);
+    });
+  });
+}
+
+tg_status tg_orient_device(tg_graph* g) {
+  return guard([&] {
+    enter(g);
+    tgb::orient_rows(g->g, 0, (uint32_t)g->g.n, g->eff, g->stream);
+    g->have_eff = true;
+  });
+}
+
+tg_status tg_count_device(tg_graph* g, uint64_t* d_total) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(d_total != nullptr, "null output");
+    cudaStream_t s = g->stream;
+    ensure_eff(g);
+    TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
+    const CsrView full = view(g->eff);
+    const uint32_t N = (uint32_t)g->g.n;
+    timed_pass(g, [&] {
+      tgb::intersect_rows(full, 0, N, full, 0, N,
+                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s);
+    });
+  });
+}
+
+double tg_last_intersect_ms(tg_graph* g) {
+  if (!g || !g->timed) return 0.0;
+  float ms = 0.f;
+  cudaSetDevice(g->device);
+  if (cudaEventSynchronize(g->ev1) != cudaSuccess) return 0.0;
+  if (cudaEventElapsedTime(&ms, g->ev0, g->ev1) != cudaSuccess) return 0.0;
+  return ms;
+}
+
+tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t rank,
+                             uint64_t* d_total) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(boundaries && p >= 1 && rank < p && d_total, "invalid argument");
+    TG_REQUIRE(boundaries[0] == 0 && boundaries[p] <= g->g.n, "invalid boundaries");
+    ensure_eff(g);
+    cudaStream_t s = g->stream;
+    const CsrView full = view(g->eff);
+    const uint32_t N = (uint32_t)g->g.n;
+    const uint32_t cb = boundaries[rank], ce = boundaries[rank + 1];
+    timed_pass(g, [&] {
+      if (ce > cb)
+        tgb::intersect_rows(full, cb, ce, full, 0, N,
+                            CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s);
+    });
+  });
+}
+
+tg_status tg_surrogate_pack_sizes(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t rank,
+                                  uint64_t* msgs_per_dest, uint64_t* words_per_dest) {
+  return guard([&] {
+    enter(g);
+    prepare_part(g, boundaries, p, rank);
+    if (msgs_per_dest) std::memcpy(msgs_per_dest, g->pack.msgs_per_dest.data(), p * 8);
+    if (words_per_dest) std::memcpy(words_per_dest, g->pack.words_per_dest.data(), p * 8);
+  });
+}
+
+tg_status tg_surrogate_pack_device(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t rank,
+                                   uint32_t* d_hdr, uint32_t* d_data) {
+  return guard([&] {
+    enter(g);
+    prepare_part(g, boundaries, p, rank);
+    g->pack.scatter(d_hdr, d_data, g->stream);
+  });
+}
+
+tg_status tg_surrogate_count_device(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t rank,
+                                    const uint32_t* d_hdr, uint64_t num_msgs, const uint32_t* d_data,
+                                    uint64_t* d_total) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(d_total != nullptr, "null output");
+    prepare_part(g, boundaries, p, rank);
+    cudaStream_t s = g->stream;
+    const uint32_t cb = boundaries[rank], ce = boundaries[rank + 1];
+    DBuf<uint64_t> moff;
+    tgb::message_offsets(d_hdr, num_msgs, moff, s);
+    const CsrView pv = view(g->part);
+    const CountOut out{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0};
+    timed_pass(g, [&] {
+      if (ce > cb) {
+        tgb::intersect_rows(pv, cb, ce, pv, cb, ce, out, g->scr, s);
+        if (num_msgs) {
+          tgb::MsgView mv{d_hdr, moff.p, d_data, num_msgs};
+          tgb::intersect_msgs(mv, pv, cb, ce, out, g->scr, s);
+        }
+      }
+    });
+    sync(g);  // moff is freed on return
+  });
+}
+
+}  // extern "C"

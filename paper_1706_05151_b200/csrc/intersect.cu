@@ -1,0 +1,366 @@
+// intersect.cu -- the hot loop: |N_v ∩ N_u| over every oriented edge v -> u.
+//
+// Reference: count_node_iterator_n (sequential.hpp:74-91) over
+// intersect_visit (intersect.hpp:15-33), the AOP rank body aop_count
+// (engines.hpp:38-54) and SurrogateCount surrogate_handle (engines.hpp:60-76),
+// with the sinks NodeTallySink (sequential.hpp:24-33) and ListSink
+// (sequential.hpp:36-46) / RankSink (engines.hpp:303-321).
+//
+// B200 design (integer set intersection; no tensor cores):
+//  * apex-centric: one warp (short N_v) or one 512-thread CTA (long N_v) owns
+//    apex v and stages N_v in shared memory once, so N_v is read from HBM once
+//    per apex instead of once per oriented edge;
+//  * the work of the apex, sum_{u in N_v} h_u elements, is flattened across
+//    the lanes: each lane takes one element x of one N_u (coalesced reads of
+//    consecutive N_u entries), finds its u by a 5-step search over the
+//    prefix of list lengths, and tests x ∈ N_v by binary search in shared
+//    memory.  A triangle (v,u,x) is found exactly once (Theorem 1).
+//  * counts are reduced with __ballot_sync/__popc and one 64-bit atomic per
+//    warp per kernel; per-node tallies fold T_v per apex and T_u per edge
+//    before touching global atomics; listing compacts found triples with one
+//    atomicAdd per warp-iteration.
+#include <cub/block/block_scan.cuh>
+
+#include "tg_internal.cuh"
+
+namespace tgb {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;  // warp path: 256 threads
+constexpr int kWCap = 64;          // apex lists up to 64 entries on the warp path
+constexpr int kBT = 512;           // CTA path threads
+constexpr int kBCap = 12288;       // CTA path: N_v entries staged in smem (48 KB)
+
+struct RowsApex {
+  CsrView view;
+  uint32_t vlo, vhi;
+  __device__ __forceinline__ uint64_t count() const { return vhi - vlo; }
+  __device__ __forceinline__ void get(uint64_t k, uint32_t& v, const uint32_t*& L,
+                                      uint32_t& hv) const {
+    v = vlo + (uint32_t)k;
+    uint64_t a = view.off[v - view.base], b = view.off[v - view.base + 1];
+    L = view.data + a;
+    hv = (uint32_t)(b - a);
+  }
+};
+
+struct MsgApex {
+  MsgView m;
+  __device__ __forceinline__ uint64_t count() const { return m.count; }
+  __device__ __forceinline__ void get(uint64_t k, uint32_t& v, const uint32_t*& L,
+                                      uint32_t& hv) const {
+    v = m.hdr[2 * k];
+    hv = m.hdr[2 * k + 1];
+    L = m.data + m.moff[k];
+  }
+};
+
+// number of elements < x in ascending a[0..n)
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ bool contains_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t i = lower_bound_u32(a, n, x);
+  return i < n && a[i] == x;
+}
+
+// largest j in [0, nb) with start[j] <= idx (start[0] == 0, nondecreasing)
+__device__ __forceinline__ int seg_of(const uint32_t* start, int nb, uint32_t idx) {
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= idx) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void emit_triple(const CountOut& out, unsigned long long pos, uint32_t a,
+                                            uint32_t b, uint32_t c) {
+  // ListSink normalisation (sequential.hpp:39-44)
+  uint32_t t;
+  if (a > b) { t = a; a = b; b = t; }
+  if (b > c) { t = b; b = c; c = t; }
+  if (a > b) { t = a; a = b; b = t; }
+  if (pos < out.cap) {
+    out.tri[3 * pos + 0] = a;
+    out.tri[3 * pos + 1] = b;
+    out.tri[3 * pos + 2] = c;
+  }
+}
+
+// ------------------------------------------------------------- warp path
+
+template <bool TALLY, bool LIST, class Apex>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
+                 uint32_t* __restrict__ big, unsigned long long* __restrict__ big_count,
+                 uint64_t big_cap) {
+  __shared__ uint32_t sNv[kWarpsPerBlock][kWCap];
+  __shared__ uint32_t sStart[kWarpsPerBlock][32];
+  __shared__ uint64_t sLo[kWarpsPerBlock][32];
+  __shared__ uint32_t sU[kWarpsPerBlock][32];
+  __shared__ unsigned sCntU[kWarpsPerBlock][32];
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const uint64_t nitems = A.count();
+  uint32_t* Nv = sNv[w];
+  unsigned long long acc = 0;
+
+  for (uint64_t k = (uint64_t)blockIdx.x * kWarpsPerBlock + w; k < nitems;
+       k += (uint64_t)gridDim.x * kWarpsPerBlock) {
+    uint32_t v, hv;
+    const uint32_t* L;
+    A.get(k, v, L, hv);
+    if (hv < 2) continue;  // a triangle needs u, w ∈ N_v
+    if (hv > kWCap) {
+      if (lane == 0) {
+        unsigned long long pos = atomicAdd(big_count, 1ull);
+        if (pos < big_cap) big[pos] = (uint32_t)k;
+      }
+      continue;
+    }
+    for (uint32_t i = lane; i < hv; i += 32) Nv[i] = L[i];
+    __syncwarp();
+    // middle-vertex range [ulo, uhi): contiguous in the ID-sorted N_v
+    uint32_t jlo = 0, jhi = 0;
+    for (uint32_t i0 = 0; i0 < hv; i0 += 32) {
+      uint32_t x = (i0 + lane < hv) ? Nv[i0 + lane] : 0xffffffffu;
+      bool in = i0 + lane < hv;
+      jlo += __popc(__ballot_sync(FULL, in && x < ulo));
+      jhi += __popc(__ballot_sync(FULL, in && x < uhi));
+    }
+    unsigned long long apex_cnt = 0;
+    for (uint32_t jb = jlo; jb < jhi; jb += 32) {
+      const int nb = (int)min(32u, jhi - jb);
+      uint32_t len = 0, u = 0;
+      uint64_t lo = 0;
+      if ((int)lane < nb) {
+        u = Nv[jb + lane];
+        uint64_t a = nu.off[u - nu.base], b = nu.off[u - nu.base + 1];
+        lo = a;
+        len = (uint32_t)(b - a);
+      }
+      uint32_t incl = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if ((int)lane >= o) incl += t;
+      }
+      const uint32_t S = __shfl_sync(FULL, incl, 31);
+      sStart[w][lane] = incl - len;
+      sLo[w][lane] = lo;
+      if (TALLY || LIST) sU[w][lane] = u;
+      if (TALLY) sCntU[w][lane] = 0;
+      __syncwarp();
+      for (uint32_t base = 0; base < S; base += 32) {
+        const uint32_t idx = base + lane;
+        bool found = false;
+        int jj = 0;
+        uint32_t x = 0;
+        if (idx < S) {
+          jj = seg_of(sStart[w], nb, idx);
+          x = nu.data[sLo[w][jj] + (idx - sStart[w][jj])];
+          found = contains_u32(Nv, hv, x);
+        }
+        const unsigned m = __ballot_sync(FULL, found);
+        apex_cnt += __popc(m);
+        if (TALLY && found) {
+          atomicAdd(&out.tally[x], 1ull);
+          atomicAdd(&sCntU[w][jj], 1u);
+        }
+        if (LIST && m) {
+          unsigned long long b0 = 0;
+          if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
+          b0 = __shfl_sync(FULL, b0, 0);
+          if (found) emit_triple(out, b0 + __popc(m & ((1u << lane) - 1u)), v, sU[w][jj], x);
+        }
+      }
+      __syncwarp();
+      if (TALLY && (int)lane < nb && sCntU[w][lane])
+        atomicAdd(&out.tally[sU[w][lane]], (unsigned long long)sCntU[w][lane]);
+      __syncwarp();
+    }
+    if (TALLY && lane == 0 && apex_cnt) atomicAdd(&out.tally[v], apex_cnt);
+    acc += apex_cnt;
+    __syncwarp();
+  }
+  if (lane == 0 && acc) atomicAdd(out.total, acc);
+}
+
+// ------------------------------------------------------------- CTA path
+
+template <bool TALLY, bool LIST, class Apex>
+__global__ void __launch_bounds__(kBT, 2)
+k_intersect_block(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
+                  const uint32_t* __restrict__ big, const unsigned long long* __restrict__ big_count,
+                  uint64_t big_cap, uint32_t bcap) {
+  extern __shared__ uint32_t sNvDyn[];
+  using Scan = cub::BlockScan<uint32_t, kBT>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ uint32_t sStart[kBT];
+  __shared__ uint64_t sLo[kBT];
+  __shared__ uint32_t sU[kBT];
+  __shared__ unsigned sCntU[kBT];
+  __shared__ uint32_t sJ[2];
+  __shared__ uint32_t sTotal;
+  __shared__ unsigned long long sApex;
+  const unsigned t = threadIdx.x, lane = t & 31;
+  const unsigned FULL = 0xffffffffu;
+  uint64_t nbig = *big_count;
+  if (nbig > big_cap) nbig = big_cap;
+  unsigned long long acc = 0;
+
+  for (uint64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    uint32_t v, hv;
+    const uint32_t* L;
+    A.get(big[bi], v, L, hv);
+    const bool in_smem = hv <= bcap;
+    const uint32_t* Nv = in_smem ? sNvDyn : L;
+    if (in_smem)
+      for (uint32_t i = t; i < hv; i += kBT) sNvDyn[i] = L[i];
+    if (t == 0) sApex = 0;
+    __syncthreads();
+    if (t == 0) {
+      sJ[0] = lower_bound_u32(Nv, hv, ulo);
+      sJ[1] = lower_bound_u32(Nv, hv, uhi);
+    }
+    __syncthreads();
+    const uint32_t jlo = sJ[0], jhi = sJ[1];
+    unsigned long long apex_cnt = 0;
+    for (uint32_t jb = jlo; jb < jhi; jb += kBT) {
+      const int nb = (int)min((uint32_t)kBT, jhi - jb);
+      uint32_t len = 0, u = 0;
+      uint64_t lo = 0;
+      if ((int)t < nb) {
+        u = Nv[jb + t];
+        uint64_t a = nu.off[u - nu.base], b = nu.off[u - nu.base + 1];
+        lo = a;
+        len = (uint32_t)(b - a);
+      }
+      uint32_t excl, S;
+      Scan(scan_tmp).ExclusiveSum(len, excl, S);
+      sStart[t] = excl;
+      sLo[t] = lo;
+      if (TALLY || LIST) sU[t] = u;
+      if (TALLY) sCntU[t] = 0;
+      __syncthreads();
+      for (uint32_t base = 0; base < S; base += kBT) {
+        const uint32_t idx = base + t;
+        bool found = false;
+        int jj = 0;
+        uint32_t x = 0;
+        if (idx < S) {
+          jj = seg_of(sStart, nb, idx);
+          x = nu.data[sLo[jj] + (idx - sStart[jj])];
+          found = contains_u32(Nv, hv, x);
+        }
+        const unsigned m = __ballot_sync(FULL, found);
+        apex_cnt += __popc(m);  // per-warp partial, summed below
+        if (TALLY && found) {
+          atomicAdd(&out.tally[x], 1ull);
+          atomicAdd(&sCntU[jj], 1u);
+        }
+        if (LIST && m) {
+          unsigned long long b0 = 0;
+          if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
+          b0 = __shfl_sync(FULL, b0, 0);
+          if (found) emit_triple(out, b0 + __popc(m & ((1u << lane) - 1u)), v, sU[jj], x);
+        }
+      }
+      __syncthreads();
+      if (TALLY && (int)t < nb && sCntU[t])
+        atomicAdd(&out.tally[sU[t]], (unsigned long long)sCntU[t]);
+      __syncthreads();
+    }
+    // apex_cnt is replicated across the lanes of each warp
+    if (lane == 0 && apex_cnt) atomicAdd(&sApex, apex_cnt);
+    __syncthreads();
+    if (t == 0) {
+      if (TALLY && sApex) atomicAdd(&out.tally[v], sApex);
+      acc += sApex;
+    }
+    __syncthreads();
+  }
+  if (t == 0 && acc) atomicAdd(out.total, acc);
+}
+
+template <bool TALLY, bool LIST, class Apex>
+void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
+                 const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+  if (!items) return;
+  scr.ensure(items, s);
+  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, sizeof(unsigned long long), s));
+  unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * 64u);
+  k_intersect_warp<TALLY, LIST, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
+      A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+  const uint32_t bcap = g_block_cap ? g_block_cap : (uint32_t)kBCap;
+  const int dyn = (int)(bcap * 4);
+  TG_CUDA(cudaFuncSetAttribute(k_intersect_block<TALLY, LIST, Apex>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  k_intersect_block<TALLY, LIST, Apex><<<148 * 2, kBT, dyn, s>>>(
+      A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, bcap);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
+template <class Apex>
+void dispatch(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
+              const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+  const bool tally = out.tally != nullptr, list = out.tri != nullptr;
+  if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s);
+  else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s);
+  else if (list) launch_pair<false, true>(A, items, nu, ulo, uhi, out, scr, s);
+  else launch_pair<false, false>(A, items, nu, ulo, uhi, out, scr, s);
+}
+
+__global__ void k_cc(const uint64_t* __restrict__ off, uint64_t n,
+                     const unsigned long long* __restrict__ tally, double* __restrict__ c) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t d = off[v + 1] - off[v];
+    double r = 0.0;
+    if (d >= 2)  // engines.hpp:428-433, IEEE-rounded mul/div, no contraction
+      r = __ddiv_rn(__dmul_rn(2.0, (double)tally[v]), __dmul_rn((double)d, (double)(d - 1)));
+    c[v] = r;
+  }
+}
+
+}  // namespace
+
+uint32_t g_block_cap = 0;
+
+void IntersectScratch::ensure(uint64_t cap, cudaStream_t s) {
+  if (big.n < cap) big.alloc(cap, s);
+  if (!big_count.n) big_count.alloc(1, s);
+}
+
+void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
+                    uint32_t uhi, const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+  RowsApex A{apex, vlo, vhi};
+  dispatch(A, (uint64_t)(vhi - vlo), nu, ulo, uhi, out, scr, s);
+}
+
+void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
+                    const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+  MsgApex A{msgs};
+  dispatch(A, msgs.count, nu, ulo, uhi, out, scr, s);
+}
+
+void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,
+                       cudaStream_t s) {
+  if (!g.n) return;
+  k_cc<<<grid_for(g.n, 256), 256, 0, s>>>(g.off.p, g.n, d_tally, d_c);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
+}  // namespace tgb

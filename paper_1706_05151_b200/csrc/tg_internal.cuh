@@ -1,0 +1,170 @@
+// tg_internal.cuh -- shared device/host plumbing for the B200 triangle library.
+//
+// Layout in HBM (one device, one graph):
+//   sym_off  uint64[n+1], sym_adj uint32[2m]   -- reference Graph (graph.hpp:16-53)
+//   deg      uint32[n]                          -- degree, the ByDegree key (order.hpp:95-104)
+//   eff_off  uint64[n+1], eff uint32[m]         -- EffectiveAdjacency (effective.hpp:17-35),
+//                                                  lists ID-sorted, oriented v -> u iff
+//                                                  (deg v, v) < (deg u, u)
+// All sizes are 64-bit; node ids are uint32 (NodeId, graph.hpp:14).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/trigraph_b200.h"
+
+namespace tgb {
+
+// Error carried from the C++ implementation to the C-ABI status codes.
+struct Error : std::runtime_error {
+  tg_status status;
+  Error(tg_status s, const std::string& what) : std::runtime_error(what), status(s) {}
+};
+
+#define TG_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      throw ::tgb::Error(_e == cudaErrorMemoryAllocation ? TG_ERR_OOM : TG_ERR_CUDA,   \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e) + " at " + \
+                             __FILE__ + ":" + std::to_string(__LINE__));               \
+  } while (0)
+
+#define TG_CHECK_LAUNCH() TG_CUDA(cudaGetLastError())
+
+#define TG_REQUIRE(cond, msg)                                   \
+  do {                                                          \
+    if (!(cond)) throw ::tgb::Error(TG_ERR_INVALID_ARGUMENT, msg); \
+  } while (0)
+
+// Device buffer owned by the library; freed stream-ordered.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = 0;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) TG_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+  }
+  void release() noexcept {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void zero() {
+    if (n) TG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+// Symmetric CSR resident on a device (reference Graph).
+struct DevGraph {
+  uint64_t n = 0, m2 = 0;  // m2 = 2m adjacency entries
+  DBuf<uint64_t> off;      // n+1
+  DBuf<uint32_t> adj;      // m2
+  DBuf<uint32_t> deg;      // n
+};
+
+// Oriented CSR (reference EffectiveAdjacency), possibly partition-local:
+// list(v) = data[off[v-base] .. off[v-base+1]) for v in [base, base+rows).
+struct DevEff {
+  uint64_t rows = 0, entries = 0;
+  uint32_t base = 0;
+  DBuf<uint64_t> off;   // rows+1
+  DBuf<uint32_t> data;  // entries
+};
+
+// Read-only view passed to kernels.
+struct CsrView {
+  const uint64_t* off;
+  const uint32_t* data;
+  uint32_t base;
+};
+
+// ---- build / orient (build.cu, orient.cu) ----
+void build_graph_device(const uint32_t* d_pairs, uint64_t E, uint64_t n_override,
+                        DevGraph& g, cudaStream_t s);
+void compute_degrees(DevGraph& g, cudaStream_t s);
+// Orient rows [vlo, vhi) of g into `out` (out.base = vlo); lists ID-sorted.
+void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s);
+void degree_rank(const DevGraph& g, uint32_t* d_rank, cudaStream_t s);
+
+// ---- costs / plan (costs.cu) ----
+// f (n), prefix (n) on device.
+void node_costs_device(const DevGraph& g, const DevEff& eff, int kind, uint64_t* d_f,
+                       uint64_t* d_prefix, cudaStream_t s);
+// boundaries (p+1) on host, from the device prefix array.
+std::vector<uint32_t> boundaries_from_prefix(const uint64_t* d_prefix, uint64_t n, uint64_t p,
+                                             cudaStream_t s);
+uint64_t ordering_cost_device(const DevGraph& g, const DevEff& eff, cudaStream_t s);
+
+// ---- intersection (intersect.cu) ----
+struct CountOut {
+  unsigned long long* total;   // device, 1 counter
+  unsigned long long* tally;   // device n or nullptr (NodeTallySink)
+  uint32_t* tri;               // device 3*cap or nullptr (ListSink)
+  unsigned long long* cursor;  // device, listing cursor
+  uint64_t cap;
+};
+
+// Apexes: either CSR rows [vlo, vhi) of `apex` or packed surrogate messages.
+struct MsgView {
+  const uint32_t* hdr;   // 2*count: (v, len)
+  const uint64_t* moff;  // count: data offset of each message
+  const uint32_t* data;
+  uint64_t count;
+};
+
+struct IntersectScratch {
+  DBuf<uint32_t> big;               // apex items too long for the warp path
+  DBuf<unsigned long long> big_count;
+  void ensure(uint64_t cap, cudaStream_t s);
+};
+
+// NodeIteratorN over apex rows [vlo, vhi) of `apex`, N_u from `nu`, middle
+// vertex u restricted to [ulo, uhi).
+void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
+                    uint32_t uhi, const CountOut& out, IntersectScratch& scr,
+                    cudaStream_t s);
+// SurrogateCount (engines.hpp:60-76) over received messages.
+void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
+                    const CountOut& out, IntersectScratch& scr, cudaStream_t s);
+
+void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,
+                       cudaStream_t s);
+
+// launch counter (kernels of ours launched), for bench's gpu_launches claim
+extern unsigned long long g_launches;
+// CTA-path shared-memory capacity in entries (0 = default); tests lower it
+// to exercise the global-memory search path on small graphs.
+extern uint32_t g_block_cap;
+
+inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 64u) {
+  uint64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace tgb

@@ -1,0 +1,397 @@
+"""Python mirror of the reference `trigraph` API over the B200 C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/trigraph/ (cited per symbol); the work runs in
+libtrigraph_b200.so on the GPU.  Deviations, all documented in DESIGN.md:
+
+* ``Graph`` is device-resident (one CUDA device per Graph).
+* The order is always ByDegree (the north_star path; order.hpp:95-104).
+* ``ExecMode`` is accepted for signature parity and ignored: device results
+  are mode-independent (acceptance.cpp:438-468).
+* ``RankStats.realized_cost`` is algorithmic work (sum of h_v + h_u over the
+  rank's oriented edges), not merge comparisons.
+* ``std::invalid_argument`` maps to ``ValueError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import TgConfig, TgRankStats, check, lib
+
+NodeId = np.uint32
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+class EngineKind(enum.IntEnum):  # engines.hpp:24
+    Sequential = 0
+    Aop = 1
+    AnopDirect = 2
+    AnopSurrogate = 3
+
+
+ENGINE_NAMES = {EngineKind.Sequential: "seq", EngineKind.Aop: "aop",
+                EngineKind.AnopDirect: "anop-direct", EngineKind.AnopSurrogate: "anop-surrogate"}
+
+
+def to_string(x) -> str:  # engines.hpp:26-34, partition.hpp:24-35
+    if isinstance(x, EngineKind):
+        return ENGINE_NAMES[x]
+    if isinstance(x, CostKind):
+        return {CostKind.Dh: "DH", CostKind.Ddh: "DDH", CostKind.Dh2: "DH2",
+                CostKind.Dpd: "DPD", CostKind.Nov: "NOV"}.get(x, x.name)
+    raise TypeError(x)
+
+
+class CostKind(enum.IntEnum):  # partition.hpp:18
+    N = 0
+    D = 1
+    Dh = 2
+    Ddh = 3
+    Dh2 = 4
+    Dpd = 5
+    Nov = 6
+
+
+class ExecMode(enum.IntEnum):  # runtime.hpp:27 (accepted, no effect on the device)
+    Interleaved = 0
+    Concurrent = 1
+
+
+class Graph:
+    """Immutable undirected simple graph in CSR form, resident on one GPU
+    (graph.hpp:19-53).  Build with :func:`build_graph` or :meth:`from_csr`."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self._h = handle
+        self.device = device
+
+    @classmethod
+    def from_csr(cls, n: int, offsets, adj, device: int = 0) -> "Graph":
+        """Adopt an already-built CSR (Graph ctor, graph.hpp:22-23)."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        a = np.ascontiguousarray(adj, dtype=np.uint32)
+        if off.shape[0] != n + 1:
+            raise ValueError("offsets must have n+1 entries")
+        h = C.c_void_p()
+        check(lib().tg_graph_from_csr(device, n, _p(off), _p(a) if a.size else None, C.byref(h)))
+        return cls(h, device)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().tg_graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _info(self):
+        n, m = C.c_uint64(), C.c_uint64()
+        check(lib().tg_graph_info(self._h, C.byref(n), C.byref(m)))
+        return n.value, m.value
+
+    def num_nodes(self) -> int:  # graph.hpp:25
+        return self._info()[0]
+
+    def num_edges(self) -> int:  # graph.hpp:26
+        return self._info()[1]
+
+    def csr(self):
+        """(offsets uint64[n+1], adj uint32[2m]) copied back to the host."""
+        n, m = self._info()
+        off = np.zeros(n + 1, dtype=np.uint64)
+        adj = np.zeros(max(2 * m, 1), dtype=np.uint32)
+        check(lib().tg_graph_csr(self._h, _p(off), _p(adj)))
+        return off, adj[: 2 * m]
+
+    def degree(self, v: int) -> int:  # graph.hpp:28
+        off, _ = self.csr()
+        return int(off[v + 1] - off[v])
+
+    def neighbors(self, v: int) -> np.ndarray:  # graph.hpp:30-32
+        off, adj = self.csr()
+        return adj[off[v]:off[v + 1]]
+
+
+def build_graph(edge_pairs, n_override: int = 0, device: int = 0) -> Graph:
+    """graph.hpp:58-85 -- drops self-loops, symmetrises, sorts and uniques on
+    the device.  ``edge_pairs``: (E, 2) uint32 array-like (host or a
+    device pointer-backed torch tensor via ``build_graph_device``)."""
+    pairs = np.ascontiguousarray(np.asarray(edge_pairs, dtype=np.uint32).reshape(-1, 2))
+    h = C.c_void_p()
+    check(lib().tg_graph_from_edges(device, _p(pairs) if pairs.size else None, pairs.shape[0],
+                                    n_override, C.byref(h)))
+    return Graph(h, device)
+
+
+def build_graph_from_pointer(ptr: int, num_pairs: int, n_override: int = 0,
+                             device: int = 0) -> Graph:
+    """build_graph from a raw (host or device) pointer to interleaved pairs."""
+    h = C.c_void_p()
+    check(lib().tg_graph_from_edges(device, C.c_void_p(ptr), num_pairs, n_override, C.byref(h)))
+    return Graph(h, device)
+
+
+@dataclass
+class OrderRank:  # order.hpp:31-35
+    rank: np.ndarray
+
+    def precedes(self, u: int, v: int) -> bool:
+        return bool(self.rank[u] < self.rank[v])
+
+
+def compute_order(g: Graph, kind: str = "by_degree") -> OrderRank:
+    """order.hpp:85-128, ByDegree only (the degree order is the north_star
+    path and provably optimal)."""
+    if kind not in ("by_degree", "ByDegree"):
+        raise ValueError("only OrderKind::by_degree() is supported on the device")
+    n = g.num_nodes()
+    r = np.zeros(max(n, 1), dtype=np.uint32)
+    check(lib().tg_compute_order(g._h, _p(r)))
+    return OrderRank(r[:n])
+
+
+@dataclass
+class EffectiveAdjacency:  # effective.hpp:17-35
+    offsets: np.ndarray
+    entries: np.ndarray
+
+    def num_nodes(self) -> int:
+        return self.offsets.shape[0] - 1
+
+    def total_entries(self) -> int:
+        return int(self.entries.shape[0])
+
+    def eff(self, v: int) -> np.ndarray:
+        return self.entries[self.offsets[v]:self.offsets[v + 1]]
+
+    def effdeg(self, v: int) -> int:
+        return int(self.offsets[v + 1] - self.offsets[v])
+
+
+def effective_adjacency(g: Graph) -> EffectiveAdjacency:
+    """effective.hpp:37-52 under the degree order (oriented on the device)."""
+    n, m = g._info()
+    off = np.zeros(n + 1, dtype=np.uint64)
+    eff = np.zeros(max(m, 1), dtype=np.uint32)
+    check(lib().tg_effective_adjacency(g._h, _p(off), _p(eff)))
+    return EffectiveAdjacency(off, eff[:m])
+
+
+def count_node_iterator_n(g: Graph) -> int:
+    """sequential.hpp:74-91 count over effective_adjacency(g, by_degree)."""
+    t = C.c_uint64()
+    check(lib().tg_count(g._h, C.byref(t)))
+    return t.value
+
+
+def ordering_cost(g: Graph) -> int:
+    """sequential.hpp:95-104 under the degree order: W = sum_v d_v * h_v."""
+    t = C.c_uint64()
+    check(lib().tg_ordering_cost(g._h, C.byref(t)))
+    return t.value
+
+
+@dataclass
+class CostVector:  # partition.hpp:38-43
+    f: np.ndarray
+    prefix: np.ndarray
+
+    def total(self) -> int:
+        return int(self.prefix[-1]) if self.prefix.size else 0
+
+
+def node_costs(g: Graph, kind: CostKind) -> CostVector:
+    """partition.hpp:45-91 (DpdVariant::EffectiveOnly)."""
+    n = g.num_nodes()
+    f = np.zeros(max(n, 1), dtype=np.uint64)
+    pre = np.zeros(max(n, 1), dtype=np.uint64)
+    check(lib().tg_node_costs(g._h, int(kind), _p(f), _p(pre)))
+    return CostVector(f[:n], pre[:n])
+
+
+@dataclass
+class PartitionPlan:  # partition.hpp:95-110
+    boundaries: np.ndarray
+
+    def ranks(self) -> int:
+        return len(self.boundaries) - 1
+
+    def core_begin(self, i: int) -> int:
+        return int(self.boundaries[i])
+
+    def core_end(self, i: int) -> int:
+        return int(self.boundaries[i + 1])
+
+    def in_core(self, i: int, v: int) -> bool:
+        return self.core_begin(i) <= v < self.core_end(i)
+
+    def owner(self, v: int) -> int:
+        inner = self.boundaries[1:-1]
+        return int(np.searchsorted(inner, v, side="right"))
+
+
+def compute_boundaries(g: Graph, kind: CostKind, p: int) -> PartitionPlan:
+    """partition.hpp:116-141 over node_costs(g, kind): exact 128-bit search."""
+    if p < 1:
+        raise ValueError("compute_boundaries: p must be >= 1")
+    b = np.zeros(p + 1, dtype=np.uint32)
+    check(lib().tg_compute_boundaries(g._h, int(kind), p, _p(b)))
+    return PartitionPlan(b)
+
+
+@dataclass
+class EngineConfig:  # engines.hpp:270-280
+    engine: EngineKind = EngineKind.Aop
+    ranks: int = 1
+    cost: CostKind = CostKind.Dpd
+    order: str = "by_degree"
+    mode: ExecMode = ExecMode.Interleaved
+    track_nodes: bool = False
+    collect_triangles: bool = False
+    boundaries: Optional[Sequence[int]] = None
+
+
+@dataclass
+class RankStats:  # engines.hpp:282-287 (+ stored_entries)
+    triangles: int = 0
+    data_sent: int = 0
+    data_recv: int = 0
+    realized_cost: int = 0
+    stored_entries: int = 0
+
+
+@dataclass
+class RunReport:  # engines.hpp:289-298
+    engine: EngineKind = EngineKind.Sequential
+    ranks: int = 1
+    cost: CostKind = CostKind.Dpd
+    total: int = 0
+    per_rank: list = field(default_factory=list)
+    boundaries: np.ndarray = None
+    node_counts: Optional[np.ndarray] = None
+    triangles_list: Optional[np.ndarray] = None
+
+
+def _cfg(cfg: EngineConfig):
+    if cfg.order not in ("by_degree", "ByDegree"):
+        raise ValueError("only OrderKind::by_degree() is supported on the device")
+    c = TgConfig()
+    c.engine = int(cfg.engine)
+    c.cost = int(cfg.cost)
+    c.ranks = int(cfg.ranks)
+    keep = None
+    if cfg.boundaries is not None:
+        keep = np.ascontiguousarray(cfg.boundaries, dtype=np.uint32)
+        p = 1 if cfg.engine == EngineKind.Sequential else int(cfg.ranks)
+        if keep.shape[0] != p + 1:
+            raise ValueError("boundaries must have ranks+1 entries")
+        c.boundaries = keep.ctypes.data
+    c.track_nodes = int(bool(cfg.track_nodes))
+    c.collect_triangles = int(bool(cfg.collect_triangles))
+    return c, keep
+
+
+def run_engine(g: Graph, cfg: EngineConfig) -> RunReport:
+    """engines.hpp:335-418.  ``triangles_list`` rows are normalised to
+    ascending ids (engines.hpp:313-319); row order is unspecified, as in the
+    reference (compare sorted)."""
+    if cfg.engine != EngineKind.Sequential and int(cfg.ranks) < 1:
+        raise ValueError("run_engine: ranks must be >= 1")
+    c, keep = _cfg(cfg)
+    p = 1 if cfg.engine == EngineKind.Sequential else int(cfg.ranks)
+    n = g.num_nodes()
+    stats = (TgRankStats * p)()
+    b = np.zeros(p + 1, dtype=np.uint32)
+    total = C.c_uint64()
+    tv = np.zeros(max(n, 1), dtype=np.uint64) if cfg.track_nodes else None
+    cap = count_node_iterator_n(g) if cfg.collect_triangles else 0
+    tri = np.zeros((max(cap, 1), 3), dtype=np.uint32) if cfg.collect_triangles else None
+    ntri = C.c_uint64()
+    check(lib().tg_run_engine(g._h, C.byref(c), C.byref(total), C.cast(stats, C.c_void_p), _p(b),
+                              _p(tv), _p(tri), cap, C.byref(ntri)))
+    del keep
+    rep = RunReport(engine=EngineKind(cfg.engine), ranks=p, cost=CostKind(cfg.cost),
+                    total=total.value, boundaries=b)
+    rep.per_rank = [RankStats(s.triangles, s.data_sent, s.data_recv, s.realized_cost,
+                              s.stored_entries) for s in stats]
+    if cfg.track_nodes:
+        rep.node_counts = tv[:n]
+    if cfg.collect_triangles:
+        rep.triangles_list = tri[: ntri.value]
+    return rep
+
+
+@dataclass
+class ClusteringResult:  # engines.hpp:203-206
+    triangles_per_node: np.ndarray
+    coefficient: np.ndarray
+
+
+def clustering_coefficients(g: Graph, cfg: EngineConfig) -> ClusteringResult:
+    """engines.hpp:422-435: per-node T_v and C_v = 2 T_v / (d (d-1)) (fp64,
+    IEEE-rounded on the device; 0 when d < 2)."""
+    if cfg.engine != EngineKind.Sequential and int(cfg.ranks) < 1:
+        raise ValueError("run_engine: ranks must be >= 1")
+    c, keep = _cfg(cfg)
+    n = g.num_nodes()
+    tv = np.zeros(max(n, 1), dtype=np.uint64)
+    cc = np.zeros(max(n, 1), dtype=np.float64)
+    check(lib().tg_clustering_coefficients(g._h, C.byref(c), _p(tv), _p(cc)))
+    del keep
+    return ClusteringResult(tv[:n], cc[:n])
+
+
+# ---------------------------------------------------------------- generators
+
+
+def _pairs_from(fn, *args) -> np.ndarray:
+    ptr = C.c_void_p()
+    cnt = C.c_uint64()
+    check(fn(*args, C.byref(ptr), C.byref(cnt)))
+    E = cnt.value
+    try:
+        if E == 0:
+            return np.zeros((0, 2), dtype=np.uint32)
+        buf = (C.c_uint32 * (2 * E)).from_address(ptr.value)
+        return np.frombuffer(buf, dtype=np.uint32).reshape(E, 2).copy()
+    finally:
+        lib().tg_free_host(ptr)
+
+
+def gen_pa(n: int, d: int, seed: int) -> np.ndarray:
+    """io.hpp:129-162 gen_pa edge stream (d = average degree, d/2 attachments)."""
+    return _pairs_from(lib().tg_gen_pa, n, d, seed)
+
+
+def gen_gnp(n: int, d: float, seed: int) -> np.ndarray:
+    """io.hpp:85-123 gen_gnp edge stream."""
+    return _pairs_from(lib().tg_gen_gnp, n, d, seed)
+
+
+def gen_gnm(n: int, m: int, seed: int) -> np.ndarray:
+    return _pairs_from(lib().tg_gen_gnm, n, m, seed)
+
+
+def gen_rmat(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int) -> np.ndarray:
+    return _pairs_from(lib().tg_gen_rmat, scale, edge_factor, a, b, c, seed)
+
+
+def gen_ws(n: int, k: int, beta: float, seed: int) -> np.ndarray:
+    return _pairs_from(lib().tg_gen_ws, n, k, beta, seed)

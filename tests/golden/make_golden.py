@@ -1,0 +1,194 @@
+"""Generate tests/golden/*.json from the UNMODIFIED reference (oracle/_ref).
+
+Run here (where /root/reference is mounted and `make -C oracle` built
+oracle/_ref/libtrigraph_ref.so):
+
+    python tests/golden/make_golden.py            # small fixtures (seconds)
+    python tests/golden/make_golden.py --full     # + full-size C1/C2 goldens
+
+Every number in the fixtures comes from the reference's own functions
+(build_graph, compute_order, effective_adjacency, count_node_iterator_n,
+node_costs, compute_boundaries, run_engine, clustering_coefficients,
+gen_pa, gen_gnp, oracles::random_graph ...) called through ref_shim.cpp.
+Large arrays are stored as sha256 digests of their little-endian bytes.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import binding as B  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+ENGINES = ["seq", "aop", "anop-direct", "anop-surrogate"]
+COSTS = list(B.COSTS)
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def engine_record(R: B.RefGraph, engine, p, cost, boundaries=None):
+    rep = R.run_engine(engine, p, cost, boundaries=boundaries, track_nodes=True,
+                       collect_triangles=True)
+    pp = 1 if engine == "seq" else p
+    return {
+        "engine": engine, "ranks": p, "cost": cost,
+        "boundaries_in": None if boundaries is None else [int(x) for x in boundaries],
+        "total": rep.total,
+        "boundaries": rep.boundaries[: pp + 1].tolist(),
+        "triangles": rep.triangles[:pp].tolist(),
+        "data_sent": rep.data_sent[:pp].tolist(),
+        "data_recv": rep.data_recv[:pp].tolist(),
+        "node_counts_sha256": digest(rep.node_counts),
+        "triangles_sha256": digest(rep.triangles_list),
+    }
+
+
+def graph_record(R: B.RefGraph, name: str, pairs=None, n_override=0, engines=True):
+    g = R.csr()
+    eoff, eff = R.effective()
+    tv, cc = R.clustering("seq", 1)
+    rec = {
+        "name": name, "n": g.n, "m": g.m,
+        "offsets_sha256": digest(g.off), "adj_sha256": digest(g.adj),
+        "rank_sha256": digest(R.degree_rank()),
+        "eff_offsets_sha256": digest(eoff), "eff_sha256": digest(eff),
+        "count": R.count(), "ordering_cost": R.ordering_cost(),
+        "node_counts_sha256": digest(tv), "cc_sha256": digest(cc),
+        "costs_sha256": {k: digest(R.node_costs(k)[0]) for k in COSTS},
+    }
+    if pairs is not None:
+        rec["pairs_sha256"] = digest(np.ascontiguousarray(pairs, dtype=np.uint32))
+        rec["n_override"] = n_override
+    if engines:
+        rec["engines"] = [engine_record(R, e, p, c) for e in ENGINES for p in (1, 2, 3, 4, 8)
+                          for c in ("N", "DPD", "NOV") if not (e == "seq" and (p > 1 or c != "DPD"))]
+    return rec
+
+
+def small():
+    fx = {}
+    # G5 (proj/tests/oracles.hpp:20-22) -- explicit values, tests read them directly
+    R = B.ref_fixture("g5")
+    g = R.csr()
+    eoff, eff = R.effective()
+    tv, cc = R.clustering("aop", 2)
+    fx["g5"] = {
+        "pairs": [[0, 1], [0, 2], [1, 2], [1, 3], [2, 3], [3, 4]],
+        "offsets": g.off.tolist(), "adj": g.adj.tolist(),
+        "rank": R.degree_rank().tolist(),
+        "eff_offsets": eoff.tolist(), "eff": eff.tolist(),
+        "count": R.count(), "ordering_cost": R.ordering_cost(),
+        "costs": {k: R.node_costs(k)[0].tolist() for k in COSTS},
+        "node_counts": tv.tolist(), "cc": cc.tolist(),
+        "plan_025": [engine_record(R, e, 2, "DPD", [0, 2, 5]) for e in ENGINES[1:]],
+        "overlap_stored_025": [R.overlap_stored([0, 2, 5], i) for i in range(2)],
+    }
+    for e in fx["g5"]["plan_025"]:
+        rr = R.run_engine(e["engine"], 2, "DPD", boundaries=[0, 2, 5], collect_triangles=True)
+        e["triangles_list"] = rr.triangles_list.tolist()
+    # complete graphs, wheels, bipartite (acceptance.cpp:239-264)
+    fx["complete"] = {n: B.ref_fixture("complete", n).count() for n in range(3, 11)}
+    fx["wheel"] = {r: B.ref_fixture("wheel", r).count() for r in range(4, 13)}
+    fx["bipartite"] = {f"{a}x{b}": B.ref_fixture("complete_bipartite", a, b).count()
+                       for a, b in ((3, 4), (5, 5), (1, 6))}
+    # K8 / NOV / surrogate / p=3 (test_engines.cpp:90-94)
+    fx["k8_nov_surrogate_p3"] = B.ref_fixture("complete", 8).run_engine(
+        "anop-surrogate", 3, "NOV").total
+    # the acceptance suite: 200 seeded graphs (acceptance.cpp:76-88)
+    suite = []
+    import ctypes as C
+    st = B.lib()
+    mt = (C.c_uint64 * 313)()
+    st.orc_mt64_seed.argtypes = [C.c_void_p, C.c_uint64]
+    st.orc_mt64_next.argtypes = [C.c_void_p]
+    st.orc_mt64_next.restype = C.c_uint64
+    st.orc_mt64_seed(C.addressof(mt), 20240201)
+    for i in range(200):
+        n = 8 + st.orc_mt64_next(C.addressof(mt)) % 93
+        density = 0.02 + 0.93 * (i / 199.0)
+        seed = st.orc_mt64_next(C.addressof(mt))
+        R = B.ref_random_graph(n, density, seed)
+        rec = {"n": int(n), "density": density, "seed": int(seed), "count": R.count(),
+               "adj_sha256": digest(R.csr().adj)}
+        if i % 10 == 0:  # per-rank records for every 10th graph
+            rec["engines"] = [engine_record(R, e, p, c) for e in ENGINES[1:] for p in (2, 3, 8)
+                              for c in ("N", "DPD", "NOV")]
+        suite.append(rec)
+    fx["acceptance_suite"] = {"seed": 20240201, "graphs": suite}
+    # per-node tallies / CC (acceptance.cpp:399-426, seed 911)
+    st.orc_mt64_seed(C.addressof(mt), 911)
+    c9 = []
+    for i in range(40):
+        n = 10 + st.orc_mt64_next(C.addressof(mt)) % 50
+        density = 0.05 + 0.02 * i
+        seed = st.orc_mt64_next(C.addressof(mt))
+        R = B.ref_random_graph(n, density, seed)
+        tv, cc = R.clustering("anop-surrogate", 3)
+        c9.append({"n": int(n), "density": density, "seed": int(seed), "node_counts": tv.tolist(),
+                   "cc": [float(x).hex() for x in cc]})
+    fx["criterion9"] = c9
+    # generator streams (io.hpp:85-162) -- digests of the reference graphs
+    fx["gen_pa"] = [dict(n=n, d=d, seed=s, **{k: v for k, v in graph_record(
+        B.ref_fixture("gen_pa", n, d, s), f"pa{n}", engines=False).items()
+        if k in ("m", "adj_sha256", "offsets_sha256", "count", "ordering_cost")})
+        for (n, d, s) in ((10000, 20, 1), (2000, 40, 7), (200000, 40, 7))]
+    fx["gen_gnp"] = [dict(n=n, d=d, seed=s, **{k: v for k, v in graph_record(
+        B.ref_fixture("gen_gnp", n, float(d), s), f"gnp{n}", engines=False).items()
+        if k in ("m", "adj_sha256", "offsets_sha256", "count")})
+        for (n, d, s) in ((2000, 20, 42), (100000, 20, 7))]
+    # a PA graph with full per-engine records at p up to 8
+    R = B.ref_fixture("gen_pa", 20000, 20, 3)
+    fx["pa20000"] = graph_record(R, "gen_pa(20000,20,3)")
+    return fx
+
+
+def full():
+    sys.path.insert(0, ROOT)
+    from paper_1706_05151_b200 import trigraph as T  # generators only (host harness)
+    fx = {}
+    t = time.time()
+    pairs = T.gen_gnm(100_000, 1_000_000, 1)
+    R = B.RefGraph.from_pairs(pairs, 100_000)
+    rec = graph_record(R, "C1 gnm(1e5,1e6,seed=1)", pairs, 100_000, engines=False)
+    rec["engines"] = [engine_record(R, e, p, "DPD") for e in ENGINES for p in (1, 8)
+                      if not (e == "seq" and p > 1)]
+    fx["C1"] = rec
+    print("C1", time.time() - t, flush=True)
+    t = time.time()
+    R = B.ref_fixture("gen_pa", 10_000_000, 40, 7)
+    g = R.csr()
+    print("C2 gen", time.time() - t, flush=True)
+    t0 = time.time()
+    cnt = R.count()
+    fx["C2"] = {"name": "C2 gen_pa(1e7,40,seed=7)", "n": g.n, "m": g.m, "count": cnt,
+                "ordering_cost": R.ordering_cost(), "count_seconds_1thread": time.time() - t0,
+                "adj_sha256": digest(g.adj), "offsets_sha256": digest(g.off)}
+    print("C2", fx["C2"], flush=True)
+    return fx
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--full", action="store_true")
+    a = ap.parse_args()
+    if not B.ref_available():
+        sys.exit("oracle/_ref not built (make -C oracle with /root/reference mounted)")
+    fx = small()
+    with open(os.path.join(OUT, "reference_small.json"), "w") as f:
+        json.dump(fx, f, indent=0, sort_keys=True)
+    print("wrote reference_small.json")
+    if a.full:
+        fx = full()
+        with open(os.path.join(OUT, "reference_full.json"), "w") as f:
+            json.dump(fx, f, indent=1, sort_keys=True)
+        print("wrote reference_full.json")
