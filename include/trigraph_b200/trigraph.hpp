@@ -1,0 +1,305 @@
+// trigraph_b200/trigraph.hpp -- header-only C++ mirror of the reference
+// `trigraph` API (/root/reference/proj/include/trigraph/) over the C ABI in
+// trigraph_b200.h.  A reference user switches by including this header and
+// linking libtrigraph_b200.so:
+//
+//   #include <trigraph_b200/trigraph.hpp>
+//   namespace trigraph = trigraph_b200;     // same names, same semantics
+//
+// Names and argument meaning follow the reference (file:line cited per
+// symbol).  Differences: Graph lives on a CUDA device; the
+// order is always ByDegree; ExecMode is accepted and ignored;
+// RankStats::realized_cost is algorithmic work, not merge comparisons;
+// effective adjacency / order helpers take the Graph (the device keeps the
+// oriented CSR cached) instead of an EffectiveAdjacency / OrderRank.
+#ifndef TRIGRAPH_B200_TRIGRAPH_HPP
+#define TRIGRAPH_B200_TRIGRAPH_HPP
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../trigraph_b200.h"
+
+namespace trigraph_b200 {
+
+using NodeId = std::uint32_t;  // graph.hpp:14
+
+namespace detail {
+inline void check(tg_status s) {
+  if (s == TG_OK) return;
+  std::string msg = tg_last_error();
+  if (s == TG_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(std::string(tg_status_string(s)) + ": " + msg);
+}
+}  // namespace detail
+
+enum class EngineKind { Sequential, Aop, AnopDirect, AnopSurrogate };  // engines.hpp:24
+enum class CostKind { N, D, Dh, Ddh, Dh2, Dpd, Nov };                  // partition.hpp:18
+namespace runtime {
+enum class ExecMode { Interleaved, Concurrent };  // runtime.hpp:27 (no effect on the device)
+}
+
+/// graph.hpp:19-53 -- immutable undirected simple graph, resident on a GPU.
+class Graph {
+ public:
+  Graph() = default;
+  /// Graph(n, offsets, adj) (graph.hpp:22-23): adopt a built CSR.
+  Graph(std::size_t n, const std::vector<std::size_t>& offsets, const std::vector<NodeId>& adj,
+        int device = 0) {
+    std::vector<std::uint64_t> off(offsets.begin(), offsets.end());
+    detail::check(tg_graph_from_csr(device, n, off.data(), adj.empty() ? nullptr : adj.data(), &h_));
+  }
+  explicit Graph(tg_graph* h) : h_(h) {}
+  Graph(const Graph&) = delete;
+  Graph& operator=(const Graph&) = delete;
+  Graph(Graph&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Graph& operator=(Graph&& o) noexcept {
+    if (this != &o) {
+      if (h_) tg_graph_free(h_);
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+  ~Graph() {
+    if (h_) tg_graph_free(h_);
+  }
+
+  std::size_t num_nodes() const { return info().first; }   // graph.hpp:25
+  std::size_t num_edges() const { return info().second; }  // graph.hpp:26
+  tg_graph* handle() const { return h_; }
+
+  /// Host copy of the CSR (offsets n+1, adjacency 2m).
+  std::pair<std::vector<std::uint64_t>, std::vector<NodeId>> csr() const {
+    auto [n, m] = info();
+    std::vector<std::uint64_t> off(n + 1);
+    std::vector<NodeId> adj(2 * m);
+    detail::check(tg_graph_csr(h_, off.data(), adj.data()));
+    return {std::move(off), std::move(adj)};
+  }
+
+ private:
+  std::pair<std::size_t, std::size_t> info() const {
+    std::uint64_t n = 0, m = 0;
+    detail::check(tg_graph_info(h_, &n, &m));
+    return {n, m};
+  }
+  tg_graph* h_ = nullptr;
+};
+
+/// graph.hpp:58-85 build_graph, on the device.
+inline Graph build_graph(const std::vector<std::pair<NodeId, NodeId>>& edge_pairs,
+                         std::size_t n_override = 0, int device = 0) {
+  std::vector<std::uint32_t> flat(2 * edge_pairs.size());
+  for (std::size_t i = 0; i < edge_pairs.size(); ++i) {
+    flat[2 * i] = edge_pairs[i].first;
+    flat[2 * i + 1] = edge_pairs[i].second;
+  }
+  tg_graph* h = nullptr;
+  detail::check(tg_graph_from_edges(device, flat.empty() ? nullptr : flat.data(), edge_pairs.size(),
+                                    n_override, &h));
+  return Graph(h);
+}
+
+/// order.hpp:31-35 / :95-104 (ByDegree).
+struct OrderRank {
+  std::vector<NodeId> rank;
+  bool precedes(NodeId u, NodeId v) const { return rank[u] < rank[v]; }
+};
+inline OrderRank compute_order(const Graph& g) {
+  OrderRank o;
+  o.rank.resize(g.num_nodes());
+  detail::check(tg_compute_order(g.handle(), o.rank.data()));
+  return o;
+}
+
+/// effective.hpp:17-52 under the degree order.
+struct EffectiveAdjacency {
+  std::vector<std::uint64_t> offsets{0};
+  std::vector<NodeId> entries;
+  std::size_t num_nodes() const { return offsets.size() - 1; }
+  std::size_t total_entries() const { return entries.size(); }
+  std::size_t effdeg(NodeId v) const { return offsets[v + 1] - offsets[v]; }
+};
+inline EffectiveAdjacency effective_adjacency(const Graph& g) {
+  EffectiveAdjacency e;
+  e.offsets.resize(g.num_nodes() + 1);
+  e.entries.resize(g.num_edges());
+  detail::check(tg_effective_adjacency(g.handle(), e.offsets.data(), e.entries.data()));
+  return e;
+}
+
+/// sequential.hpp:74-91 (count only).
+inline std::uint64_t count_node_iterator_n(const Graph& g) {
+  std::uint64_t t = 0;
+  detail::check(tg_count(g.handle(), &t));
+  return t;
+}
+
+/// sequential.hpp:95-104 under the degree order.
+inline std::uint64_t ordering_cost(const Graph& g) {
+  std::uint64_t c = 0;
+  detail::check(tg_ordering_cost(g.handle(), &c));
+  return c;
+}
+
+/// partition.hpp:38-91.
+struct CostVector {
+  std::vector<std::uint64_t> f, prefix;
+  std::uint64_t total() const { return prefix.empty() ? 0 : prefix.back(); }
+};
+inline CostVector node_costs(const Graph& g, CostKind kind) {
+  CostVector c;
+  c.f.resize(g.num_nodes());
+  c.prefix.resize(g.num_nodes());
+  detail::check(tg_node_costs(g.handle(), static_cast<int32_t>(kind), c.f.data(), c.prefix.data()));
+  return c;
+}
+
+/// partition.hpp:95-141.
+struct PartitionPlan {
+  std::vector<NodeId> boundaries;
+  std::size_t ranks() const { return boundaries.size() - 1; }
+  NodeId core_begin(std::size_t i) const { return boundaries[i]; }
+  NodeId core_end(std::size_t i) const { return boundaries[i + 1]; }
+  bool in_core(std::size_t i, NodeId v) const { return v >= core_begin(i) && v < core_end(i); }
+  std::size_t owner(NodeId v) const {
+    std::size_t lo = 1, hi = boundaries.size() - 1;
+    while (lo < hi) {
+      std::size_t mid = (lo + hi) / 2;
+      if (boundaries[mid] <= v) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo - 1;
+  }
+};
+inline PartitionPlan compute_boundaries(const Graph& g, CostKind kind, std::size_t p) {
+  if (p == 0) throw std::invalid_argument("compute_boundaries: p must be >= 1");
+  PartitionPlan plan;
+  plan.boundaries.resize(p + 1);
+  detail::check(tg_compute_boundaries(g.handle(), static_cast<int32_t>(kind), p,
+                                      plan.boundaries.data()));
+  return plan;
+}
+
+/// engines.hpp:270-298.
+struct EngineConfig {
+  EngineKind engine = EngineKind::Aop;
+  std::size_t ranks = 1;
+  CostKind cost = CostKind::Dpd;
+  runtime::ExecMode mode = runtime::ExecMode::Interleaved;
+  bool track_nodes = false;
+  bool collect_triangles = false;
+  std::optional<std::vector<NodeId>> boundaries;
+};
+
+struct RankStats {
+  std::uint64_t triangles = 0, data_sent = 0, data_recv = 0, realized_cost = 0,
+                stored_entries = 0;
+};
+
+struct RunReport {
+  EngineKind engine = EngineKind::Sequential;
+  std::size_t ranks = 1;
+  CostKind cost = CostKind::Dpd;
+  std::uint64_t total = 0;
+  std::vector<RankStats> per_rank;
+  std::vector<NodeId> boundaries;
+  std::vector<std::uint64_t> node_counts;
+  std::vector<std::array<NodeId, 3>> triangles_list;
+};
+
+namespace detail {
+inline tg_config to_c(const EngineConfig& cfg) {
+  tg_config c{};
+  c.engine = static_cast<int32_t>(cfg.engine);
+  c.cost = static_cast<int32_t>(cfg.cost);
+  c.ranks = cfg.ranks;
+  c.boundaries = cfg.boundaries ? cfg.boundaries->data() : nullptr;
+  c.track_nodes = cfg.track_nodes;
+  c.collect_triangles = cfg.collect_triangles;
+  return c;
+}
+}  // namespace detail
+
+/// engines.hpp:335-418 run_engine.
+inline RunReport run_engine(const Graph& g, const EngineConfig& cfg) {
+  const std::size_t p = cfg.engine == EngineKind::Sequential ? 1 : cfg.ranks;
+  if (p == 0) throw std::invalid_argument("run_engine: ranks must be >= 1");
+  if (cfg.boundaries && cfg.boundaries->size() != p + 1)
+    throw std::invalid_argument("run_engine: boundaries must have ranks+1 entries");
+  tg_config c = detail::to_c(cfg);
+  RunReport rep;
+  rep.engine = cfg.engine;
+  rep.ranks = p;
+  rep.cost = cfg.cost;
+  std::vector<tg_rank_stats> st(p);
+  rep.boundaries.resize(p + 1);
+  if (cfg.track_nodes) rep.node_counts.resize(g.num_nodes());
+  std::uint64_t cap = cfg.collect_triangles ? count_node_iterator_n(g) : 0, got = 0;
+  std::vector<NodeId> flat(3 * cap);
+  detail::check(tg_run_engine(g.handle(), &c, &rep.total, st.data(), rep.boundaries.data(),
+                              cfg.track_nodes ? rep.node_counts.data() : nullptr,
+                              cfg.collect_triangles ? flat.data() : nullptr, cap, &got));
+  for (const auto& s : st)
+    rep.per_rank.push_back({s.triangles, s.data_sent, s.data_recv, s.realized_cost,
+                            s.stored_entries});
+  if (cfg.collect_triangles) {
+    rep.triangles_list.resize(got);
+    for (std::uint64_t k = 0; k < got; ++k)
+      rep.triangles_list[k] = {flat[3 * k], flat[3 * k + 1], flat[3 * k + 2]};
+  }
+  return rep;
+}
+
+/// engines.hpp:203-206, 422-435.
+struct ClusteringResult {
+  std::vector<std::uint64_t> triangles_per_node;
+  std::vector<double> coefficient;
+};
+inline ClusteringResult clustering_coefficients(const Graph& g, EngineConfig cfg) {
+  const std::size_t p = cfg.engine == EngineKind::Sequential ? 1 : cfg.ranks;
+  if (p == 0) throw std::invalid_argument("run_engine: ranks must be >= 1");
+  cfg.track_nodes = true;
+  tg_config c = detail::to_c(cfg);
+  ClusteringResult r;
+  r.triangles_per_node.resize(g.num_nodes());
+  r.coefficient.resize(g.num_nodes());
+  detail::check(tg_clustering_coefficients(g.handle(), &c, r.triangles_per_node.data(),
+                                           r.coefficient.data()));
+  return r;
+}
+
+/// io.hpp:129-162 gen_pa (host, bit-identical edge stream).
+inline std::vector<std::pair<NodeId, NodeId>> gen_pa_edges(std::size_t n, std::size_t d,
+                                                           std::uint64_t seed) {
+  std::uint32_t* p = nullptr;
+  std::uint64_t E = 0;
+  detail::check(tg_gen_pa(n, d, seed, &p, &E));
+  std::vector<std::pair<NodeId, NodeId>> out(E);
+  for (std::uint64_t i = 0; i < E; ++i) out[i] = {p[2 * i], p[2 * i + 1]};
+  tg_free_host(p);
+  return out;
+}
+inline Graph gen_pa(std::size_t n, std::size_t d, std::uint64_t seed, int device = 0) {
+  return build_graph(gen_pa_edges(n, d, seed), n, device);
+}
+
+inline const char* to_string(EngineKind e) {  // engines.hpp:26-34
+  switch (e) {
+    case EngineKind::Sequential: return "seq";
+    case EngineKind::Aop: return "aop";
+    case EngineKind::AnopDirect: return "anop-direct";
+    case EngineKind::AnopSurrogate: return "anop-surrogate";
+  }
+  return "?";
+}
+
+}  // namespace trigraph_b200
+
+#endif  // TRIGRAPH_B200_TRIGRAPH_HPP

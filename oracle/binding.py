@@ -45,6 +45,7 @@ def lib():
             "orc_degree_rank": (None, [u64, vp, vp]),
             "orc_effective": (u64, [u64, vp, vp, vp, vp, C.POINTER(vp)]),
             "orc_count": (u64, [u64, vp, vp, vp, vp, u64]),
+            "orc_count_range": (u64, [u64, vp, vp, u64, u64]),
             "orc_ordering_cost": (u64, [u64, vp, vp, vp]),
             "orc_node_costs": (None, [u64, vp, vp, vp, vp, i32, vp, vp]),
             "orc_compute_boundaries": (i32, [vp, u64, u64, vp]),

@@ -167,6 +167,23 @@ uint64_t orc_count(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
   return total;
 }
 
+/* NodeIteratorN restricted to apexes [vlo, vhi) (the AOP rank body's loop,
+ * engines.hpp:38-54, over the full oriented lists). */
+uint64_t orc_count_range(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
+                         uint64_t vlo, uint64_t vhi) {
+  (void)n;
+  uint64_t total = 0;
+  for (uint64_t v = vlo; v < vhi; ++v) {
+    const uint32_t* nv = eff + eoff[v];
+    uint64_t hv = eoff[v + 1] - eoff[v];
+    for (uint64_t k = 0; k < hv; ++k) {
+      uint32_t u = nv[k];
+      total += merge_emit(nv, hv, eff + eoff[u], eoff[u + 1] - eoff[u], NULL, (uint32_t)v, u);
+    }
+  }
+  return total;
+}
+
 /* sequential.hpp:95-104 ordering_cost = sum_v d_v * effdeg_v. */
 uint64_t orc_ordering_cost(uint64_t n, const uint64_t* off, const uint32_t* adj,
                            const uint32_t* rank) {

@@ -44,6 +44,10 @@ uint64_t orc_effective(uint64_t n, const uint64_t* off, const uint32_t* adj,
 uint64_t orc_count(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
                    uint64_t* tally, uint32_t* tri, uint64_t tri_cap);
 
+/* count_node_iterator_n restricted to apexes [vlo, vhi). */
+uint64_t orc_count_range(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
+                         uint64_t vlo, uint64_t vhi);
+
 /* sequential.hpp:95-104 ordering_cost under the degree order. */
 uint64_t orc_ordering_cost(uint64_t n, const uint64_t* off, const uint32_t* adj,
                            const uint32_t* rank);

@@ -71,7 +71,7 @@ using tgb::CsrView;
 using tgb::DBuf;
 using tgb::DevEff;
 
-CsrView view(const DevEff& e) { return CsrView{e.off.p, e.data.p, e.base}; }
+CsrView view(const DevEff& e) { return CsrView{e.desc.p, e.data.p, e.base}; }
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
@@ -107,6 +107,12 @@ tg_graph* new_graph(int device) {
   TG_CUDA(cudaGetDeviceCount(&count));
   TG_REQUIRE(device >= 0 && device < count, "invalid CUDA device ordinal");
   TG_CUDA(cudaSetDevice(device));
+  // keep freed stream-ordered allocations in the pool instead of returning
+  // them to the driver at every synchronisation (per-step scratch buffers)
+  cudaMemPool_t pool;
+  TG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = UINT64_MAX;
+  TG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   auto* g = new tg_graph;
   g->device = device;
   TG_CUDA(cudaStreamCreateWithFlags(&g->own, cudaStreamNonBlocking));
@@ -118,7 +124,7 @@ tg_graph* new_graph(int device) {
 
 void ensure_eff(tg_graph* g) {
   if (!g->have_eff) {
-    tgb::orient_rows(g->g, 0, (uint32_t)g->g.n, g->eff, g->stream);
+    tgb::orient_full(g->g, g->eff, g->stream);
     g->have_eff = true;
   }
 }
@@ -189,13 +195,15 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
   const uint32_t N = (uint32_t)n;
 
   if (cfg.engine == TG_ENGINE_SEQ) {
-    timed_pass(g, [&] { tgb::intersect_rows(full, 0, N, full, 0, N, out_for(0), g->scr, s); });
+    timed_pass(g, [&] { tgb::intersect_rows(full, 0, N, full, 0, N, out_for(0), g->scr, s, g->eff.data.n, true);
+    });
     R.per_rank[0].stored_entries = g->eff.entries;
   } else if (cfg.engine == TG_ENGINE_AOP || cfg.engine == TG_ENGINE_ANOP_DIRECT) {
     timed_pass(g, [&] {
       for (uint64_t i = 0; i < p; ++i)
         if (b[i + 1] > b[i])
-          tgb::intersect_rows(full, b[i], b[i + 1], full, 0, N, out_for(i), g->scr, s);
+          tgb::intersect_rows(full, b[i], b[i + 1], full, 0, N, out_for(i), g->scr, s,
+                              g->eff.data.n, true);
     });
     if (cfg.engine == TG_ENGINE_AOP) {
       for (uint64_t i = 0; i < p; ++i)
@@ -207,13 +215,8 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
         R.per_rank[i].data_sent = req[i] + rep[i];
         R.per_rank[i].data_recv = req[i] + rep[i];
       }
-      for (uint64_t i = 0; i < p; ++i) {
-        uint64_t ob[2];
-        download(&ob[0], g->eff.off.p + b[i], 1, s);
-        download(&ob[1], g->eff.off.p + b[i + 1], 1, s);
-        sync(g);
-        R.per_rank[i].stored_entries = ob[1] - ob[0];
-      }
+      for (uint64_t i = 0; i < p; ++i)
+        R.per_rank[i].stored_entries = tgb::sum_lens(g->eff, b[i], b[i + 1], s);
     }
   } else {  // ANOP surrogate
     std::vector<DevEff> parts(p);
@@ -269,9 +272,10 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
       for (uint64_t j = 0; j < p; ++j) {
         if (b[j + 1] <= b[j]) continue;
         const CsrView pv = view(parts[j]);
-        tgb::intersect_rows(pv, b[j], b[j + 1], pv, b[j], b[j + 1], out_for(j), g->scr, s);
+        tgb::intersect_rows(pv, b[j], b[j + 1], pv, b[j], b[j + 1], out_for(j), g->scr, s,
+                            parts[j].data.n, false);
         tgb::MsgView mv{rh[j].p, moff[j].p, rd[j].p, rmsgs[j]};
-        tgb::intersect_msgs(mv, pv, b[j], b[j + 1], out_for(j), g->scr, s);
+        tgb::intersect_msgs(mv, pv, b[j], b[j + 1], out_for(j), g->scr, s, parts[j].data.n);
       }
     });
   }
@@ -297,7 +301,8 @@ uint64_t seq_count(tg_graph* g) {
   const CsrView full = view(g->eff);
   const uint32_t N = (uint32_t)g->g.n;
   timed_pass(g, [&] {
-    tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, g->scr, s);
+    tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, g->scr, s,
+                        g->eff.data.n, true);
   });
   unsigned long long h = 0;
   download(&h, ctr.p, 1, s);
@@ -396,7 +401,8 @@ tg_status tg_graph_free(tg_graph* g) {
     {
       // release buffers on the library stream before destroying it
       g->g.off.release(); g->g.adj.release(); g->g.deg.release();
-      g->eff.off.release(); g->eff.data.release();
+      g->eff.off.release(); g->eff.data.release(); g->eff.desc.release();
+      g->part.desc.release();
       g->scr.big.release(); g->scr.big_count.release();
       g->part.off.release(); g->part.data.release();
       g->pack.desc.release(); g->pack.doff.release();
@@ -438,7 +444,7 @@ tg_status tg_set_stream(tg_graph* g, void* stream) {
       // re-home them so later frees order after work on the new stream.
       auto rehome = [&](auto& buf) { buf.s = ns; };
       rehome(g->g.off); rehome(g->g.adj); rehome(g->g.deg);
-      rehome(g->eff.off); rehome(g->eff.data);
+      rehome(g->eff.off); rehome(g->eff.data); rehome(g->eff.desc); rehome(g->part.desc);
       rehome(g->scr.big); rehome(g->scr.big_count);
       rehome(g->part.off); rehome(g->part.data);
       rehome(g->pack.desc); rehome(g->pack.doff);
@@ -461,8 +467,10 @@ tg_status tg_effective_adjacency(tg_graph* g, uint64_t* offsets, uint32_t* eff) 
   return guard([&] {
     enter(g);
     ensure_eff(g);
-    download(offsets, g->eff.off.p, g->g.n + 1, g->stream);
-    download(eff, g->eff.data.p, g->eff.entries, g->stream);
+    DevEff c;  // compact copy of the (gappy) resident orientation
+    tgb::compact_eff(g->eff, c, g->stream);
+    download(offsets, c.off.p, g->g.n + 1, g->stream);
+    download(eff, c.data.p, c.entries, g->stream);
     sync(g);
   });
 }
@@ -581,14 +589,15 @@ tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
     TG_REQUIRE(d_total != nullptr, "null output");
     cudaStream_t s = g->stream;
     // orientation: effective_adjacency (effective.hpp:37-52), rebuilt
-    tgb::orient_rows(g->g, 0, (uint32_t)g->g.n, g->eff, s);
+    tgb::orient_full(g->g, g->eff, s);
     g->have_eff = true;
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
     const CsrView full = view(g->eff);
     const uint32_t N = (uint32_t)g->g.n;
     timed_pass(g, [&] {
       tgb::intersect_rows(full, 0, N, full, 0, N,
-                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s);
+                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
+                          g->eff.data.n, true);
     });
   });
 }
@@ -596,7 +605,7 @@ tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
 tg_status tg_orient_device(tg_graph* g) {
   return guard([&] {
     enter(g);
-    tgb::orient_rows(g->g, 0, (uint32_t)g->g.n, g->eff, g->stream);
+    tgb::orient_full(g->g, g->eff, g->stream);
     g->have_eff = true;
   });
 }
@@ -612,7 +621,8 @@ tg_status tg_count_device(tg_graph* g, uint64_t* d_total) {
     const uint32_t N = (uint32_t)g->g.n;
     timed_pass(g, [&] {
       tgb::intersect_rows(full, 0, N, full, 0, N,
-                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s);
+                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
+                          g->eff.data.n, true);
     });
   });
 }
@@ -640,7 +650,8 @@ tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p
     timed_pass(g, [&] {
       if (ce > cb)
         tgb::intersect_rows(full, cb, ce, full, 0, N,
-                            CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s);
+                            CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
+                          g->eff.data.n, true);
     });
   });
 }
@@ -679,10 +690,10 @@ tg_status tg_surrogate_count_device(tg_graph* g, const uint32_t* boundaries, uin
     const CountOut out{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0};
     timed_pass(g, [&] {
       if (ce > cb) {
-        tgb::intersect_rows(pv, cb, ce, pv, cb, ce, out, g->scr, s);
+        tgb::intersect_rows(pv, cb, ce, pv, cb, ce, out, g->scr, s, g->part.data.n, false);
         if (num_msgs) {
           tgb::MsgView mv{d_hdr, moff.p, d_data, num_msgs};
-          tgb::intersect_msgs(mv, pv, cb, ce, out, g->scr, s);
+          tgb::intersect_msgs(mv, pv, cb, ce, out, g->scr, s, g->part.data.n);
         }
       }
     });

@@ -56,7 +56,8 @@ k_surr_runs(CsrView part, uint32_t cb, uint32_t ce, const uint32_t* __restrict__
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < (uint64_t)(ce - cb);
        r += warps) {
     const uint32_t v = cb + (uint32_t)r;
-    const uint64_t a = part.off[v - part.base], e = part.off[v - part.base + 1];
+    const uint64_t dsc = part.desc[v - part.base];
+    const uint64_t a = desc_start(dsc), e = a + desc_len(dsc);
     uint64_t wpos = EMIT ? r_or_off[r] : 0;
     uint32_t prev = 0xffffffffu;  // owner of the previous element
     uint64_t c = 0;
@@ -84,7 +85,7 @@ __global__ void k_desc_lens(const uint64_t* __restrict__ desc, uint64_t M, CsrVi
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < M;
        k += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t v = (uint32_t)desc[k], j = (uint32_t)(desc[k] >> 32);
-    const uint64_t h = part.off[v - part.base + 1] - part.off[v - part.base];
+    const uint64_t h = desc_len(part.desc[v - part.base]);
     lens[k] = h;
     atomicAdd(&per_dest_msgs[j], 1ull);
     atomicAdd(&per_dest_words[j], (unsigned long long)h);
@@ -98,7 +99,8 @@ __global__ void k_scatter(const uint64_t* __restrict__ desc, uint64_t M, CsrView
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < M; k += warps) {
     const uint32_t v = (uint32_t)desc[k];
-    const uint64_t a = part.off[v - part.base], e = part.off[v - part.base + 1];
+    const uint64_t dsc = part.desc[v - part.base];
+    const uint64_t a = desc_start(dsc), e = a + desc_len(dsc);
     if (lane == 0) {
       hdr[2 * k] = v;
       hdr[2 * k + 1] = (uint32_t)(e - a);
@@ -115,13 +117,16 @@ __global__ void k_hdr_lens(const uint32_t* __restrict__ hdr, uint64_t M, uint64_
 }
 
 // AOP storage: flag halo vertices (off-core members of core lists) ...
-__global__ void k_mark_halo(CsrView eff, uint32_t cb, uint32_t ce, uint8_t* __restrict__ flag) {
+__global__ void k_mark_halo(CsrView eff, uint32_t cb, uint32_t ce, uint8_t* __restrict__ flag,
+                            unsigned long long* __restrict__ core_entries) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < (uint64_t)(ce - cb);
        r += warps) {
     const uint32_t v = cb + (uint32_t)r;
-    for (uint64_t k = eff.off[v] + lane; k < eff.off[v + 1]; k += 32) {
+    const uint64_t dsc = eff.desc[v], a = desc_start(dsc), e = a + desc_len(dsc);
+    if (lane == 0 && e > a) atomicAdd(core_entries, (unsigned long long)(e - a));
+    for (uint64_t k = a + lane; k < e; k += 32) {
       uint32_t u = eff.data[k];
       if (u < cb || u >= ce) flag[u] = 1;
     }
@@ -136,7 +141,8 @@ __global__ void k_count_trimmed(CsrView eff, uint64_t n, uint32_t cb, uint32_t c
   uint64_t s = 0;
   for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < n; w += warps) {
     if (!flag[w]) continue;
-    for (uint64_t k = eff.off[w] + lane; k < eff.off[w + 1]; k += 32) {
+    const uint64_t dsc = eff.desc[w], a = desc_start(dsc), e = a + desc_len(dsc);
+    for (uint64_t k = a + lane; k < e; k += 32) {
       uint32_t x = eff.data[k];
       if ((x >= cb && x < ce) || flag[x]) ++s;
     }
@@ -158,7 +164,8 @@ k_direct_msgs(CsrView eff, uint64_t n, const uint32_t* __restrict__ gb, uint32_t
   for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
     const uint32_t ov = owner_of(sb, p, (uint32_t)v);
     unsigned long long mine = 0;
-    for (uint64_t k = eff.off[v] + lane; k < eff.off[v + 1]; k += 32) {
+    const uint64_t dsc = eff.desc[v], a = desc_start(dsc), e = a + desc_len(dsc);
+    for (uint64_t k = a + lane; k < e; k += 32) {
       uint32_t ou = owner_of(sb, p, eff.data[k]);
       if (ou != ov) {
         ++mine;
@@ -248,20 +255,13 @@ void message_offsets(const uint32_t* d_hdr, uint64_t M, DBuf<uint64_t>& moff, cu
 }
 
 uint64_t overlap_stored_entries(CsrView eff, uint64_t n, uint32_t cb, uint32_t ce, cudaStream_t s) {
-  uint64_t core = 0;
-  {
-    uint64_t ob[2];
-    TG_CUDA(cudaMemcpyAsync(&ob[0], eff.off + cb, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaMemcpyAsync(&ob[1], eff.off + ce, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaStreamSynchronize(s));
-    core = ob[1] - ob[0];
-  }
-  if (ce <= cb || !n) return core;
+  if (ce <= cb || !n) return 0;
   DBuf<uint8_t> flag(n, s);
   flag.zero();
   DBuf<unsigned long long> acc(1, s);
   acc.zero();
-  k_mark_halo<<<grid_for((uint64_t)(ce - cb) * 32, 256, 148u * 32u), 256, 0, s>>>(eff, cb, ce, flag.p);
+  k_mark_halo<<<grid_for((uint64_t)(ce - cb) * 32, 256, 148u * 32u), 256, 0, s>>>(eff, cb, ce, flag.p,
+                                                                                 acc.p);
   TG_CHECK_LAUNCH();
   k_count_trimmed<<<grid_for(n * 32, 256, 148u * 32u), 256, 0, s>>>(eff, n, cb, ce, flag.p, acc.p);
   TG_CHECK_LAUNCH();
@@ -269,7 +269,7 @@ uint64_t overlap_stored_entries(CsrView eff, uint64_t n, uint32_t cb, uint32_t c
   unsigned long long h = 0;
   TG_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
-  return core + h;
+  return h;
 }
 
 void direct_messages(CsrView eff, uint64_t n, const std::vector<uint32_t>& b,

@@ -20,6 +20,7 @@
 //    before touching global atomics; listing compacts found triples with one
 //    atomicAdd per warp-iteration.
 #include <cub/block/block_scan.cuh>
+#include <type_traits>
 
 #include "tg_internal.cuh"
 
@@ -38,9 +39,9 @@ struct RowsApex {
   __device__ __forceinline__ void get(uint64_t k, uint32_t& v, const uint32_t*& L,
                                       uint32_t& hv) const {
     v = vlo + (uint32_t)k;
-    uint64_t a = view.off[v - view.base], b = view.off[v - view.base + 1];
-    L = view.data + a;
-    hv = (uint32_t)(b - a);
+    const uint64_t d = view.desc[v - view.base];
+    L = view.data + desc_start(d);
+    hv = desc_len(d);
   }
 };
 
@@ -98,21 +99,62 @@ __device__ __forceinline__ void emit_triple(const CountOut& out, unsigned long l
 
 // ------------------------------------------------------------- warp path
 
-template <bool TALLY, bool LIST, class Apex>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+constexpr int kBmWords = 256;   // per-warp membership filter: 8192 bits
+constexpr int kTblWords = 32;   // segment-start table window: 1024 items
+constexpr int kUnroll = 4;      // chunks (of 32 items) in flight per warp
+// Sentinel for "no item": 0xffffffff is never a NodeId of an n < 2^32 graph.
+constexpr uint32_t kNoItem = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t bm_hash(uint32_t x) { return (x * 0x9E3779B1u) >> 19; }
+
+// Branch-free membership in an ascending shared-memory array of n <= 64.
+__device__ __forceinline__ bool contains_small(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t pos = 0;
+#pragma unroll
+  for (uint32_t step = 32; step > 0; step >>= 1)
+    if (pos + step <= n && a[pos + step - 1] < x) pos += step;
+  return pos < n && a[pos] == x;
+}
+
+// One warp per apex v (h_v <= kWCap).
+//  * N_v is staged in shared memory together with an 8192-bit hashed filter.
+//  * The apex's work, sum_{u in N_v} h_u elements, is flattened over the
+//    lanes in 32-item chunks; kUnroll chunks are loaded before any is used.
+//  * A lane finds the segment (middle vertex u) of its item from a per-window
+//    bit table of segment starts: jj = #starts <= item - 1 (one broadcast LDS,
+//    two POPCs), then fetches its element x of N_u (consecutive lanes read
+//    consecutive addresses of the same list).
+//  * x is rejected by one filter probe; only when some lane of the warp hits
+//    (true members + ~0.3% false positives per lane) does the warp take the
+//    rare path: a branch-free 6-step search of N_v confirms, and __ballot /
+//    __popc count the triangles.
+// FILTER restricts the middle vertex to [ulo, uhi) (SurrogateCount's core
+// range); WIDE selects 64-bit element indexing (> 2^32 list entries).
+template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 6)
 k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                  uint32_t* __restrict__ big, unsigned long long* __restrict__ big_count,
                  uint64_t big_cap) {
+  using Adj = typename std::conditional<WIDE, long long, uint32_t>::type;
   __shared__ uint32_t sNv[kWarpsPerBlock][kWCap];
-  __shared__ uint32_t sStart[kWarpsPerBlock][32];
-  __shared__ uint64_t sLo[kWarpsPerBlock][32];
+  __shared__ uint32_t sBm[kWarpsPerBlock][kBmWords];
+  __shared__ uint32_t sTbl[kWarpsPerBlock][kTblWords + kUnroll];
+  __shared__ Adj sAdj[kWarpsPerBlock][32];
+  __shared__ uint32_t sSt[kWarpsPerBlock][32];
   __shared__ uint32_t sU[kWarpsPerBlock][32];
   __shared__ unsigned sCntU[kWarpsPerBlock][32];
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned le_mask = (2u << lane) - 1u;  // lane 31 -> 0xffffffff
   const uint64_t nitems = A.count();
   uint32_t* Nv = sNv[w];
+  uint32_t* Bm = sBm[w];
+  uint32_t* Tbl = sTbl[w];
   unsigned long long acc = 0;
+#pragma unroll
+  for (int i = 0; i < kBmWords / 32; ++i) Bm[lane + 32 * i] = 0;
+  __syncwarp();
 
   for (uint64_t k = (uint64_t)blockIdx.x * kWarpsPerBlock + w; k < nitems;
        k += (uint64_t)gridDim.x * kWarpsPerBlock) {
@@ -127,68 +169,120 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       }
       continue;
     }
-    for (uint32_t i = lane; i < hv; i += 32) Nv[i] = L[i];
-    __syncwarp();
-    // middle-vertex range [ulo, uhi): contiguous in the ID-sorted N_v
-    uint32_t jlo = 0, jhi = 0;
+    // stage N_v + filter; with FILTER count the middle-vertex range [jlo, jhi)
+    uint32_t jlo = 0, jhi = hv;
+    if (FILTER) jhi = 0;
     for (uint32_t i0 = 0; i0 < hv; i0 += 32) {
-      uint32_t x = (i0 + lane < hv) ? Nv[i0 + lane] : 0xffffffffu;
-      bool in = i0 + lane < hv;
-      jlo += __popc(__ballot_sync(FULL, in && x < ulo));
-      jhi += __popc(__ballot_sync(FULL, in && x < uhi));
+      const bool in = i0 + lane < hv;
+      uint32_t x = 0;
+      if (in) {
+        x = L[i0 + lane];
+        Nv[i0 + lane] = x;
+        const uint32_t h = bm_hash(x);
+        atomicOr(&Bm[h >> 5], 1u << (h & 31));
+      }
+      if (FILTER) {
+        jlo += __popc(__ballot_sync(FULL, in && x < ulo));
+        jhi += __popc(__ballot_sync(FULL, in && x < uhi));
+      }
     }
-    unsigned long long apex_cnt = 0;
+    __syncwarp();
+    uint32_t apex_cnt = 0;
     for (uint32_t jb = jlo; jb < jhi; jb += 32) {
-      const int nb = (int)min(32u, jhi - jb);
+      const uint32_t j = jb + lane;
       uint32_t len = 0, u = 0;
       uint64_t lo = 0;
-      if ((int)lane < nb) {
-        u = Nv[jb + lane];
-        uint64_t a = nu.off[u - nu.base], b = nu.off[u - nu.base + 1];
-        lo = a;
-        len = (uint32_t)(b - a);
+      if (j < jhi) {
+        u = Nv[j];
+        const uint64_t d = nu.desc[u - nu.base];
+        lo = desc_start(d);
+        len = desc_len(d);
       }
       uint32_t incl = len;
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(FULL, incl, o);
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
         if ((int)lane >= o) incl += t;
       }
       const uint32_t S = __shfl_sync(FULL, incl, 31);
-      sStart[w][lane] = incl - len;
-      sLo[w][lane] = lo;
-      if (TALLY || LIST) sU[w][lane] = u;
+      if (S == 0) continue;
+      // compact the non-empty segments: segment c lives in lane c
+      const unsigned ne = __ballot_sync(FULL, len > 0);
+      const uint32_t nseg = __popc(ne);
+      if (len > 0) {
+        const uint32_t c = __popc(ne & lt_mask);
+        sAdj[w][c] = (Adj)((long long)lo - (long long)(incl - len));
+        sSt[w][c] = incl - len;
+        if (TALLY || LIST) sU[w][c] = u;
+      }
       if (TALLY) sCntU[w][lane] = 0;
       __syncwarp();
-      for (uint32_t base = 0; base < S; base += 32) {
-        const uint32_t idx = base + lane;
-        bool found = false;
-        int jj = 0;
-        uint32_t x = 0;
-        if (idx < S) {
-          jj = seg_of(sStart[w], nb, idx);
-          x = nu.data[sLo[w][jj] + (idx - sStart[w][jj])];
-          found = contains_u32(Nv, hv, x);
+      const bool has = lane < nseg;
+      const Adj my_adj = has ? sAdj[w][lane] : (Adj)0;
+      const uint32_t my_st = has ? sSt[w][lane] : 0xffffffffu;
+      uint32_t cnt = 0;  // segment starts before the current chunk
+      for (uint32_t w0 = 0; w0 < S; w0 += 32 * kTblWords) {
+        Tbl[lane] = 0;
+        if (lane < kUnroll) Tbl[kTblWords + lane] = 0;
+        __syncwarp();
+        if (has && my_st >= w0 && my_st < w0 + 32 * kTblWords)
+          atomicOr(&Tbl[(my_st - w0) >> 5], 1u << (my_st & 31));
+        __syncwarp();
+        const uint32_t wend = min(S, w0 + 32 * kTblWords);
+        for (uint32_t base0 = w0; base0 < wend; base0 += 32 * kUnroll) {
+          uint32_t xs[kUnroll], jjs[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const uint32_t base = base0 + 32 * q;
+            const uint32_t word = Tbl[(base - w0) >> 5];  // padded: 0 past the window
+            const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
+            cnt += __popc(word);
+            const Adj a = __shfl_sync(FULL, my_adj, jj);  // srcLane is taken mod 32
+            const uint32_t idx = base + lane;
+            jjs[q] = jj;
+            if (WIDE) xs[q] = idx < S ? __ldg(nu.data + ((long long)a + idx)) : kNoItem;
+            else xs[q] = idx < S ? __ldg(nu.data + (uint32_t)((uint32_t)a + idx)) : kNoItem;
+          }
+          // branch-free filter probes, one vote for all kUnroll chunks
+          unsigned hits = 0;
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const uint32_t h = bm_hash(xs[q]);
+            const unsigned bit = (Bm[h >> 5] >> (h & 31)) & (unsigned)(xs[q] != kNoItem);
+            hits |= bit << q;
+          }
+          if (!__any_sync(FULL, hits != 0)) continue;
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const uint32_t x = xs[q];
+            const bool hit = (hits >> q) & 1u;
+            if (__any_sync(FULL, hit)) {  // rare: confirm against N_v
+              const bool found = hit && contains_small(Nv, hv, x);
+              const unsigned m = __ballot_sync(FULL, found);
+              apex_cnt += __popc(m);
+              if (TALLY && found) {
+                atomicAdd(&out.tally[x], 1ull);
+                atomicAdd(&sCntU[w][jjs[q]], 1u);
+              }
+              if (LIST && m) {
+                unsigned long long b0 = 0;
+                if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
+                b0 = __shfl_sync(FULL, b0, 0);
+                if (found) emit_triple(out, b0 + __popc(m & lt_mask), v, sU[w][jjs[q]], x);
+              }
+            }
+          }
         }
-        const unsigned m = __ballot_sync(FULL, found);
-        apex_cnt += __popc(m);
-        if (TALLY && found) {
-          atomicAdd(&out.tally[x], 1ull);
-          atomicAdd(&sCntU[w][jj], 1u);
-        }
-        if (LIST && m) {
-          unsigned long long b0 = 0;
-          if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
-          b0 = __shfl_sync(FULL, b0, 0);
-          if (found) emit_triple(out, b0 + __popc(m & ((1u << lane) - 1u)), v, sU[w][jj], x);
-        }
+        __syncwarp();
       }
-      __syncwarp();
-      if (TALLY && (int)lane < nb && sCntU[w][lane])
+      if (TALLY && has && sCntU[w][lane])
         atomicAdd(&out.tally[sU[w][lane]], (unsigned long long)sCntU[w][lane]);
       __syncwarp();
     }
-    if (TALLY && lane == 0 && apex_cnt) atomicAdd(&out.tally[v], apex_cnt);
+    if (TALLY && lane == 0 && apex_cnt) atomicAdd(&out.tally[v], (unsigned long long)apex_cnt);
     acc += apex_cnt;
+    // clear the filter words this apex touched
+    for (uint32_t i = lane; i < hv; i += 32) Bm[bm_hash(Nv[i]) >> 5] = 0;
     __syncwarp();
   }
   if (lane == 0 && acc) atomicAdd(out.total, acc);
@@ -240,9 +334,9 @@ k_intersect_block(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       uint64_t lo = 0;
       if ((int)t < nb) {
         u = Nv[jb + t];
-        uint64_t a = nu.off[u - nu.base], b = nu.off[u - nu.base + 1];
-        lo = a;
-        len = (uint32_t)(b - a);
+        const uint64_t d = nu.desc[u - nu.base];
+        lo = desc_start(d);
+        len = desc_len(d);
       }
       uint32_t excl, S;
       Scan(scan_tmp).ExclusiveSum(len, excl, S);
@@ -291,17 +385,30 @@ k_intersect_block(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   if (t == 0 && acc) atomicAdd(out.total, acc);
 }
 
-template <bool TALLY, bool LIST, class Apex>
-void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
+template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
+void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
                  const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
-  if (!items) return;
-  scr.ensure(items, s);
-  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, sizeof(unsigned long long), s));
   unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * 64u);
-  k_intersect_warp<TALLY, LIST, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
+  k_intersect_warp<TALLY, LIST, FILTER, WIDE, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
       A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n);
   TG_CHECK_LAUNCH();
   ++g_launches;
+}
+
+template <bool TALLY, bool LIST, class Apex>
+void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
+                 const CountOut& out, IntersectScratch& scr, cudaStream_t s, bool filter,
+                 bool wide) {
+  if (!items) return;
+  scr.ensure(items, s);
+  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, sizeof(unsigned long long), s));
+  if (filter) {
+    if (wide) launch_warp<TALLY, LIST, true, true>(A, items, nu, ulo, uhi, out, scr, s);
+    else launch_warp<TALLY, LIST, true, false>(A, items, nu, ulo, uhi, out, scr, s);
+  } else {
+    if (wide) launch_warp<TALLY, LIST, false, true>(A, items, nu, ulo, uhi, out, scr, s);
+    else launch_warp<TALLY, LIST, false, false>(A, items, nu, ulo, uhi, out, scr, s);
+  }
   const uint32_t bcap = g_block_cap ? g_block_cap : (uint32_t)kBCap;
   const int dyn = (int)(bcap * 4);
   TG_CUDA(cudaFuncSetAttribute(k_intersect_block<TALLY, LIST, Apex>,
@@ -314,12 +421,14 @@ void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
 
 template <class Apex>
 void dispatch(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
-              const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+              const CountOut& out, IntersectScratch& scr, cudaStream_t s, bool filter,
+              uint64_t data_entries) {
   const bool tally = out.tally != nullptr, list = out.tri != nullptr;
-  if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s);
-  else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s);
-  else if (list) launch_pair<false, true>(A, items, nu, ulo, uhi, out, scr, s);
-  else launch_pair<false, false>(A, items, nu, ulo, uhi, out, scr, s);
+  const bool wide = data_entries >= (1ull << 32);
+  if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
+  else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
+  else if (list) launch_pair<false, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
+  else launch_pair<false, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
 }
 
 __global__ void k_cc(const uint64_t* __restrict__ off, uint64_t n,
@@ -344,15 +453,17 @@ void IntersectScratch::ensure(uint64_t cap, cudaStream_t s) {
 }
 
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
-                    uint32_t uhi, const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+                    uint32_t uhi, const CountOut& out, IntersectScratch& scr, cudaStream_t s,
+                    uint64_t nu_entries, bool unrestricted) {
   RowsApex A{apex, vlo, vhi};
-  dispatch(A, (uint64_t)(vhi - vlo), nu, ulo, uhi, out, scr, s);
+  dispatch(A, (uint64_t)(vhi - vlo), nu, ulo, uhi, out, scr, s, !unrestricted, nu_entries);
 }
 
 void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
-                    const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
+                    const CountOut& out, IntersectScratch& scr, cudaStream_t s,
+                    uint64_t nu_entries) {
   MsgApex A{msgs};
-  dispatch(A, msgs.count, nu, ulo, uhi, out, scr, s);
+  dispatch(A, msgs.count, nu, ulo, uhi, out, scr, s, true, nu_entries);
 }
 
 void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,

@@ -94,9 +94,11 @@ __global__ void k_degrees(const uint64_t* __restrict__ off, uint64_t n, uint32_t
 
 // ---------------------------------------------------------------- orientation
 
-// G lanes per vertex.  Pass 0 counts h_v; pass 1 writes the ID-sorted N_v
-// (ballot prefix keeps adjacency order).
-template <int G, bool FILL>
+// G lanes per vertex.  MODE 0 counts h_v; MODE 1 writes the ID-sorted N_v
+// compactly at cnt_or_off[v-vlo] (ballot prefix keeps adjacency order);
+// MODE 2 (gappy, single pass) writes N_v into the first h_v slots of v's
+// symmetric slot range and the packed descriptor (sym_off[v], h_v).
+template <int G, int MODE>
 __global__ void __launch_bounds__(256)
 k_orient(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
          const uint32_t* __restrict__ deg, uint32_t vlo, uint32_t vhi,
@@ -105,40 +107,42 @@ k_orient(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
   const unsigned sub = lane & (G - 1);
   const unsigned gbase = lane & ~(G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+  const unsigned lt = (1u << lane) - 1u;
   const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
   for (uint64_t g = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / G;; g += groups) {
     // all lanes of a warp iterate together so __ballot_sync stays legal
-    uint64_t vv = vlo + g;
-    bool active = vv < vhi;
+    const uint64_t vv = vlo + g;
+    const bool active = vv < vhi;
     if (__all_sync(0xffffffffu, !active)) break;
-    uint32_t v = active ? (uint32_t)vv : 0;
-    uint64_t b = active ? off[v] : 0, e = active ? off[v + 1] : 0;
-    uint32_t dv = active ? deg[v] : 0;
-    uint64_t wpos = FILL && active ? cnt_or_off[v - vlo] : 0;
+    const uint32_t v = active ? (uint32_t)vv : 0;
+    const uint64_t b = active ? off[v] : 0, e = active ? off[v + 1] : 0;
+    const uint32_t dv = active ? deg[v] : 0;
+    uint64_t wpos = 0;
+    if (MODE == 1 && active) wpos = cnt_or_off[v - vlo];
+    if (MODE == 2) wpos = b;
     uint64_t c = 0;
-    uint64_t len = e - b;
-    // uniform trip count across the warp
-    uint64_t mylen = len, maxlen = len;
+    const uint64_t len = e - b;
+    uint64_t maxlen = len;  // uniform trip count across the warp
     for (int o = 16; o > 0; o >>= 1) {
-      uint64_t t = __shfl_xor_sync(0xffffffffu, maxlen, o);
+      const uint64_t t = __shfl_xor_sync(0xffffffffu, maxlen, o);
       maxlen = t > maxlen ? t : maxlen;
     }
     for (uint64_t k0 = 0; k0 < maxlen; k0 += G) {
-      uint64_t k = k0 + sub;
+      const uint64_t k = k0 + sub;
       bool keep = false;
       uint32_t u = 0;
-      if (k < mylen) {
+      if (k < len) {
         u = adj[b + k];
         keep = precedes(dv, v, deg[u], u);
       }
-      unsigned bal = __ballot_sync(0xffffffffu, keep) & gmask;
-      if (FILL && keep) {
-        unsigned before = __popc(bal & ((1u << lane) - 1u));
-        eff[wpos + c + before] = u;
-      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep) & gmask;
+      if (MODE != 0 && keep) eff[wpos + c + __popc(bal & lt)] = u;
       c += __popc(bal);
     }
-    if (!FILL && active && sub == 0) cnt_or_off[v - vlo] = c;
+    if (active && sub == 0) {
+      if (MODE == 0) cnt_or_off[v - vlo] = c;
+      if (MODE == 2) cnt_or_off[v] = make_desc(b, c);
+    }
   }
 }
 
@@ -147,7 +151,7 @@ void launch_orient(const DevGraph& g, uint32_t vlo, uint32_t vhi, uint64_t* cnt,
                    uint32_t* eff, cudaStream_t s) {
   uint64_t rows = vhi - vlo;
   unsigned grid = grid_for(rows * G, 256, 148u * 32u);
-  k_orient<G, false><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, vlo, vhi, cnt, nullptr);
+  k_orient<G, 0><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, vlo, vhi, cnt, nullptr);
   TG_CHECK_LAUNCH();
   ++g_launches;
   // exclusive scan into off_out[0..rows]
@@ -157,19 +161,311 @@ void launch_orient(const DevGraph& g, uint32_t vlo, uint32_t vhi, uint64_t* cnt,
       return cub::DeviceScan::InclusiveSum(t, b, cnt, off_out + 1, (int64_t)rows, s);
     });
     g_launches += 2;  // CUB decoupled look-back scan: init + scan kernels
-    k_orient<G, true><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, vlo, vhi, off_out, eff);
+    k_orient<G, 1><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, vlo, vhi, off_out, eff);
     TG_CHECK_LAUNCH();
     ++g_launches;
   }
 }
 
+template <int G>
+void launch_orient_gappy(const DevGraph& g, uint64_t* desc, uint32_t* eff, cudaStream_t s) {
+  unsigned grid = grid_for(g.n * G, 256, 148u * 32u);
+  k_orient<G, 2><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, 0, (uint32_t)g.n, desc, eff);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
+// ---- compact orientation, tile-streamed (the hot path) -------------------
+//
+// One warp per tile of 32 consecutive vertices.  The tile's adjacency
+// [off[v0], off[v0+32]) is contiguous, so the warp streams it in coalesced
+// 32-item chunks (kOUnroll chunks in flight), finds each item's source vertex
+// from a bit table of segment starts, and tests precedes(v, u) against the
+// L2-resident degree array.  Two modes, so tiles never wait on each other:
+//   COUNT: h_v of each vertex (cumulative kept count at segment ends);
+//   FILL : after a scan of h, kept item number k of the tile goes to
+//          eff[eoff[v0] + k] -- stream order is vertex order and ID order
+//          within a vertex, i.e. exactly the compact EffectiveAdjacency.
+constexpr int kOWarps = 8;
+constexpr int kOTbl = 32;       // table window: 1024 items
+constexpr int kOUnroll = 4;
+
+constexpr uint32_t kOBig = 256;  // degree above which a vertex leaves its tile
+
+// Tiles skip "big" vertices (degree > kOBig): their items are removed from the
+// tile's item space (so a hub cannot stall one warp), and they are handled by
+// k_orient_big (32 lanes per vertex) from a queue the COUNT pass fills.
+// Tiles are claimed dynamically (tile_ctr).
+template <bool FILL>
+__global__ void __launch_bounds__(kOWarps * 32, 5)
+k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+               const uint32_t* __restrict__ deg, uint64_t n, uint64_t* __restrict__ cnt_or_eoff,
+               uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff,
+               unsigned long long* __restrict__ tile_ctr, uint32_t* __restrict__ bigq,
+               unsigned long long* __restrict__ bigq_n, uint32_t* __restrict__ kmask) {
+  __shared__ uint32_t sTbl[kOWarps][kOTbl + kOUnroll];
+  __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
+  __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
+  uint32_t* Tbl = sTbl[w];
+  const uint64_t ntiles = (n + 31) / 32;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(tile_ctr, 1ull);
+    t = __shfl_sync(FULL, t, 0);
+    if (t >= ntiles) break;
+    const uint64_t v0 = t * 32;
+    const uint64_t v = v0 + lane;
+    const bool valid = v < n;
+    const uint64_t my_b = valid ? off[v] : 0, my_e = valid ? off[v + 1] : 0;
+    const uint32_t my_dv = valid ? deg[v] : 0;
+    const uint64_t tile_b = __shfl_sync(FULL, my_b, 0);
+    const uint32_t len = (uint32_t)(my_e - my_b);
+    const bool big = len > kOBig;
+    if (!FILL && big) bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
+    const uint32_t elen = big ? 0u : len;  // length in the tile's item space
+    uint32_t est = elen;                   // -> exclusive prefix of elen
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(FULL, est, o);
+      if ((int)lane >= o) est += x;
+    }
+    const uint32_t S = __shfl_sync(FULL, est, 31);  // tile items (big vertices excluded)
+    est -= elen;
+    if (S == 0) {
+      if (valid && !big) {
+        if (!FILL) cnt_or_eoff[v] = 0;
+        else edesc[v] = make_desc(cnt_or_eoff[v], 0);
+      }
+      continue;
+    }
+    // FILL: tile-relative output base of each segment, minus its items before
+    uint32_t obase = 0;
+    uint64_t out_b = 0;
+    if (FILL) {
+      uint64_t my_o = valid ? cnt_or_eoff[v] : 0;
+      out_b = __shfl_sync(FULL, my_o, 0);
+      uint32_t hk = 0;  // kept entries of this (non-big) vertex
+      if (valid && !big) hk = (uint32_t)(cnt_or_eoff[v + 1] - my_o);
+      uint32_t kst = hk;  // exclusive prefix of non-big kept counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(FULL, kst, o);
+        if ((int)lane >= o) kst += x;
+      }
+      kst -= hk;
+      obase = (uint32_t)(my_o - out_b) - kst;
+      if (valid && !big) edesc[v] = make_desc(my_o, hk);
+    }
+    // compact the non-empty segments (non-big vertices with adjacency)
+    const unsigned ne = __ballot_sync(FULL, elen > 0);
+    const uint32_t nseg = __popc(ne);
+    if (elen > 0) {
+      const uint32_t c = __popc(ne & lt_mask);
+      sV[w][c] = (uint32_t)v;
+      sDv[w][c] = my_dv;
+      sSt[w][c] = est;
+      sAs[w][c] = (uint32_t)(my_b - tile_b) - est;  // item -> adjacency index shift
+      if (FILL) sSh[w][c] = obase;                  // item's kept rank -> output shift
+    }
+    __syncwarp();
+    const bool has = lane < nseg;
+    const uint32_t c_v = has ? sV[w][lane] : 0, c_dv = has ? sDv[w][lane] : 0;
+    const uint32_t c_st = has ? sSt[w][lane] : 0xffffffffu;
+    const uint32_t c_sh = (FILL && has) ? sSh[w][lane] : 0;
+    const uint32_t c_ash = has ? sAs[w][lane] : 0;
+    uint32_t c_end = __shfl_down_sync(FULL, c_st, 1);  // end of compacted segment `lane`
+    if (lane + 1 >= nseg) c_end = S;
+    uint32_t kept = 0, cnt = 0;
+    for (uint32_t w0 = 0; w0 < S; w0 += 32 * kOTbl) {
+      Tbl[lane] = 0;
+      if (lane < kOUnroll) Tbl[kOTbl + lane] = 0;
+      __syncwarp();
+      if (has && c_st >= w0 && c_st < w0 + 32 * kOTbl)
+        atomicOr(&Tbl[(c_st - w0) >> 5], 1u << (c_st & 31));
+      __syncwarp();
+      const uint32_t wend = min(S, w0 + 32 * kOTbl);
+      for (uint32_t base0 = w0; base0 < wend; base0 += 32 * kOUnroll) {
+        uint32_t us[kOUnroll], jjs[kOUnroll], kms[kOUnroll];
+#pragma unroll
+        for (int q = 0; q < kOUnroll; ++q) {
+          const uint32_t base = base0 + 32 * q;
+          const uint32_t word = Tbl[(base - w0) >> 5];  // padded: 0 past the window
+          const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
+          jjs[q] = jj;
+          cnt += __popc(word);
+          const uint32_t idx = base + lane;
+          const uint32_t ash = __shfl_sync(FULL, c_ash, jj);
+          if (FILL) {
+            // keep decisions recorded by the COUNT pass: bits [tile_b+base, +32)
+            const uint64_t pos = tile_b + base;
+            const uint32_t sh = (uint32_t)(pos & 31);
+            const uint32_t lo = kmask[pos >> 5], hi = sh ? kmask[(pos >> 5) + 1] : 0u;
+            const uint32_t vm = base >= wend ? 0u
+                                : (wend - base >= 32 ? FULL : ((1u << (wend - base)) - 1u));
+            kms[q] = (sh ? ((lo >> sh) | (hi << (32 - sh))) : lo) & vm;
+            us[q] = ((kms[q] >> lane) & 1u) ? adj[tile_b + ash + idx] : 0u;
+          } else {
+            us[q] = idx < wend ? adj[tile_b + ash + idx] : 0u;
+          }
+        }
+        if (FILL) {
+#pragma unroll
+          for (int q = 0; q < kOUnroll; ++q) {
+            const uint32_t km = kms[q];
+            const uint32_t ob = __shfl_sync(FULL, c_sh, jjs[q]);
+            if ((km >> lane) & 1u) eff[out_b + ob + kept + __popc(km & lt_mask)] = us[q];
+            kept += __popc(km);
+          }
+        } else {
+          uint32_t dus[kOUnroll];
+#pragma unroll
+          for (int q = 0; q < kOUnroll; ++q)
+            dus[q] = (base0 + 32 * q + lane < wend) ? deg[us[q]] : 0u;
+#pragma unroll
+          for (int q = 0; q < kOUnroll; ++q) {
+            const uint32_t base = base0 + 32 * q;
+            const uint32_t idx = base + lane;
+            const uint32_t jj = jjs[q];
+            const uint32_t sv = __shfl_sync(FULL, c_v, jj);
+            const uint32_t sdv = __shfl_sync(FULL, c_dv, jj);
+            const bool keep = idx < wend && precedes(sdv, sv, dus[q], us[q]);
+            const unsigned km = __ballot_sync(FULL, keep);
+            const uint32_t send = __shfl_sync(FULL, c_end, jj);
+            if (idx < wend && idx + 1 == send) sCum[w][jj] = kept + __popc(km & le_mask);
+            if (lane == 0 && km) {  // record the decisions for the FILL pass
+              const uint64_t pos = tile_b + base;
+              const uint32_t sh = (uint32_t)(pos & 31);
+              atomicOr(&kmask[pos >> 5], km << sh);
+              if (sh) atomicOr(&kmask[(pos >> 5) + 1], km >> (32 - sh));
+            }
+            kept += __popc(km);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+    if (!FILL && valid && !big) {
+      uint32_t h = 0;
+      if (elen > 0) {
+        const uint32_t c = __popc(ne & lt_mask);
+        h = sCum[w][c] - (c ? sCum[w][c - 1] : 0u);
+      }
+      cnt_or_eoff[v] = h;
+    }
+    __syncwarp();
+  }
+}
+
+// Big vertices: 32 lanes per vertex over a device-side queue.  COUNT writes
+// h_v; FILL writes N_v at eoff[v] in adjacency order (ballot prefix).
+template <bool FILL>
+__global__ void __launch_bounds__(256)
+k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+             const uint32_t* __restrict__ deg, const uint32_t* __restrict__ bigq,
+             const unsigned long long* __restrict__ bigq_n, uint64_t* __restrict__ cnt_or_eoff,
+             uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff,
+             uint32_t* __restrict__ kmask) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint64_t nq = *bigq_n;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // keep bits at the real adjacency positions (a separate mask from the tiles')
+  auto mask_at = [&](uint64_t pos, uint64_t e) -> uint32_t {
+    const uint32_t sh = (uint32_t)(pos & 31);
+    const uint32_t lo = kmask[pos >> 5], hi = sh ? kmask[(pos >> 5) + 1] : 0u;
+    const uint32_t m = sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
+    return e - pos >= 32 ? m : (m & ((1u << (e - pos)) - 1u));
+  };
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nq; i += warps) {
+    const uint32_t v = bigq[i];
+    const uint64_t b = off[v], e = off[v + 1];
+    const uint32_t dv = deg[v];
+    const uint64_t ob = FILL ? cnt_or_eoff[v] : 0;
+    uint64_t c = 0;
+    for (uint64_t k0 = b; k0 < e; k0 += 64) {
+      const uint64_t k1 = k0 + lane, k2 = k0 + 32 + lane;
+      unsigned m1, m2;
+      uint32_t u1, u2;
+      if (FILL) {
+        m1 = mask_at(k0, e);
+        m2 = k0 + 32 < e ? mask_at(k0 + 32, e) : 0u;
+        u1 = ((m1 >> lane) & 1u) ? adj[k1] : 0u;
+        u2 = ((m2 >> lane) & 1u) ? adj[k2] : 0u;
+        if ((m1 >> lane) & 1u) eff[ob + c + __popc(m1 & lt_mask)] = u1;
+        if ((m2 >> lane) & 1u) eff[ob + c + __popc(m1) + __popc(m2 & lt_mask)] = u2;
+      } else {
+        u1 = k1 < e ? adj[k1] : 0u;
+        u2 = k2 < e ? adj[k2] : 0u;
+        const uint32_t d1 = k1 < e ? deg[u1] : 0u, d2 = k2 < e ? deg[u2] : 0u;
+        const bool p1 = k1 < e && precedes(dv, v, d1, u1);
+        const bool p2 = k2 < e && precedes(dv, v, d2, u2);
+        m1 = __ballot_sync(0xffffffffu, p1);
+        m2 = __ballot_sync(0xffffffffu, p2);
+        if (lane < 2) {
+          const unsigned mm = lane ? m2 : m1;
+          const uint64_t pos = k0 + 32 * lane;
+          if (mm) {
+            const uint32_t sh = (uint32_t)(pos & 31);
+            atomicOr(&kmask[pos >> 5], mm << sh);
+            if (sh) atomicOr(&kmask[(pos >> 5) + 1], mm >> (32 - sh));
+          }
+        }
+      }
+      c += __popc(m1) + __popc(m2);
+    }
+    if (lane == 0) {
+      if (FILL) edesc[v] = make_desc(ob, c);
+      else cnt_or_eoff[v] = c;
+    }
+  }
+}
+
+__global__ void k_desc_from_off(const uint64_t* __restrict__ off, uint64_t rows,
+                                uint64_t* __restrict__ desc) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    desc[r] = make_desc(off[r], off[r + 1] - off[r]);
+}
+
+__global__ void k_desc_lens(const uint64_t* __restrict__ desc, uint64_t rows,
+                            uint64_t* __restrict__ lens) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    lens[r] = desc_len(desc[r]);
+}
+
+__global__ void k_gather_compact(CsrView in, uint64_t rows, const uint64_t* __restrict__ off,
+                                 uint32_t* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+    const uint64_t d = in.desc[r];
+    const uint64_t st = desc_start(d), o = off[r];
+    for (uint32_t i = lane; i < desc_len(d); i += 32) out[o + i] = in.data[st + i];
+  }
+}
+
+__global__ void k_sum_lens(const uint64_t* __restrict__ desc, uint64_t lo, uint64_t hi,
+                           unsigned long long* __restrict__ acc) {
+  uint64_t s = 0;
+  for (uint64_t r = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < hi;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    s += desc_len(desc[r]);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(acc, (unsigned long long)s);
+}
+
 // ---------------------------------------------------------------- costs
 
-__global__ void k_cost_simple(const uint64_t* __restrict__ eoff, const uint32_t* __restrict__ deg,
+__global__ void k_cost_simple(const uint64_t* __restrict__ edesc, const uint32_t* __restrict__ deg,
                               uint64_t n, int kind, uint64_t* __restrict__ f) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t d = deg[v], h = eoff[v + 1] - eoff[v], r = 0;
+    uint64_t d = deg[v], h = desc_len(edesc[v]), r = 0;
     switch (kind) {
       case TG_COST_N: r = 1; break;
       case TG_COST_D: r = d; break;
@@ -187,20 +483,20 @@ __global__ void k_cost_simple(const uint64_t* __restrict__ eoff, const uint32_t*
 template <bool NOV>
 __global__ void __launch_bounds__(256)
 k_cost_sum(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-           const uint32_t* __restrict__ deg, const uint64_t* __restrict__ eoff,
-           const uint32_t* __restrict__ eff, uint64_t n, uint64_t* __restrict__ f) {
+           const uint32_t* __restrict__ deg, CsrView eff, uint64_t n, uint64_t* __restrict__ f) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-    uint64_t hv = eoff[v + 1] - eoff[v];
+    const uint64_t dsc = eff.desc[v];
+    const uint64_t hv = desc_len(dsc);
     uint64_t b, e;
     if (NOV) { b = off[v]; e = off[v + 1]; }
-    else { b = eoff[v]; e = eoff[v + 1]; }
-    uint32_t dv = deg[v];
+    else { b = desc_start(dsc); e = b + hv; }
+    const uint32_t dv = deg[v];
     uint64_t s = 0;
     for (uint64_t k = b + lane; k < e; k += 32) {
-      uint32_t u = NOV ? adj[k] : eff[k];
-      if (!NOV || precedes(deg[u], u, dv, (uint32_t)v)) s += hv + (eoff[u + 1] - eoff[u]);
+      const uint32_t u = NOV ? adj[k] : eff.data[k];
+      if (!NOV || precedes(deg[u], u, dv, (uint32_t)v)) s += hv + desc_len(eff.desc[u]);
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) f[v] = s;
@@ -228,12 +524,12 @@ __global__ void k_boundaries(const uint64_t* __restrict__ prefix, uint64_t n, ui
   b[j] = (uint32_t)lo;
 }
 
-__global__ void k_ordering_cost(const uint32_t* __restrict__ deg, const uint64_t* __restrict__ eoff,
+__global__ void k_ordering_cost(const uint32_t* __restrict__ deg, const uint64_t* __restrict__ edesc,
                                 uint64_t n, unsigned long long* __restrict__ out) {
   uint64_t s = 0;
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x)
-    s += (uint64_t)deg[v] * (eoff[v + 1] - eoff[v]);
+    s += (uint64_t)deg[v] * desc_len(edesc[v]);
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, (unsigned long long)s);
 }
@@ -321,39 +617,140 @@ void compute_degrees(DevGraph& g, cudaStream_t s) {
   }
 }
 
-// effective.hpp:37-52 for rows [vlo, vhi).  No host sync: sum of h over all
-// rows is m when vlo = 0 and vhi = n; for a partial range the caller learns
-// `entries` from the scanned offsets (one 8-byte D2H).
+// effective.hpp:37-52 for rows [vlo, vhi), compact layout (partitions, the
+// exported EffectiveAdjacency).  One host sync for the entry count.
 void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s) {
-  uint64_t rows = vhi - vlo;
+  const uint64_t rows = vhi - vlo;
   out.rows = rows;
   out.base = vlo;
+  out.compact = true;
   out.off.alloc(rows + 1, s);
+  out.desc.alloc(rows ? rows : 1, s);
   DBuf<uint64_t> cnt(rows ? rows : 1, s);
-  uint64_t entries;
-  bool full = (vlo == 0 && vhi == g.n);
-  // data buffer: exact size for the full graph (sum h = m), else bound by the
-  // symmetric entries of the range
-  uint64_t bound = full ? g.m2 / 2 : 0;
-  if (!full) {
-    uint64_t ob[2];
-    TG_CUDA(cudaMemcpyAsync(&ob[0], g.off.p + vlo, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaMemcpyAsync(&ob[1], g.off.p + vhi, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaStreamSynchronize(s));
-    bound = ob[1] - ob[0];
-  }
+  uint64_t ob[2] = {0, 0};
+  TG_CUDA(cudaMemcpyAsync(&ob[0], g.off.p + vlo, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaMemcpyAsync(&ob[1], g.off.p + vhi, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  const uint64_t bound = ob[1] - ob[0];  // symmetric entries of the range
   out.data.alloc(bound ? bound : 1, s);
-  uint64_t avg = g.n ? g.m2 / g.n : 0;
+  const uint64_t avg = g.n ? g.m2 / g.n : 0;
   if (avg <= 12) launch_orient<8>(g, vlo, vhi, cnt.p, out.off.p, out.data.p, s);
   else if (avg <= 24) launch_orient<16>(g, vlo, vhi, cnt.p, out.off.p, out.data.p, s);
   else launch_orient<32>(g, vlo, vhi, cnt.p, out.off.p, out.data.p, s);
-  if (full) {
-    entries = g.m2 / 2;
-  } else {
-    TG_CUDA(cudaMemcpyAsync(&entries, out.off.p + rows, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaStreamSynchronize(s));
+  if (rows) {
+    k_desc_from_off<<<grid_for(rows, 256), 256, 0, s>>>(out.off.p, rows, out.desc.p);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
   }
+  uint64_t entries = 0;
+  TG_CUDA(cudaMemcpyAsync(&entries, out.off.p + rows, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
   out.entries = entries;
+}
+
+// effective.hpp:37-52 for the whole graph (the hot path): tile-streamed
+// count -> CUB scan -> tile-streamed fill, compact layout, no host sync
+// (sum h_v = m is known).
+void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
+  TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
+  out.rows = g.n;
+  out.base = 0;
+  out.compact = true;
+  out.entries = g.m2 / 2;
+  const uint64_t m = g.m2 / 2;
+  if (out.desc.n < (g.n ? g.n : 1)) out.desc.alloc(g.n ? g.n : 1, s);
+  if (out.off.n < g.n + 1) out.off.alloc(g.n + 1, s);
+  if (out.data.n < (m ? m : 1)) out.data.alloc(m ? m : 1, s);
+  if (!g.n) {
+    TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
+    return;
+  }
+  const uint64_t ntiles = (g.n + 31) / 32;
+  const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
+  DBuf<uint64_t> cnt(g.n, s);
+  DBuf<uint32_t> bigq(g.n, s);
+  DBuf<unsigned long long> ctr(3, s);  // tile counters (count, fill), big-queue size
+  ctr.zero();
+  // keep-decision bitmasks (tiles: compressed item space; big: real positions)
+  const uint64_t mwords = g.m2 / 32 + 8;
+  DBuf<uint32_t> kmask(2 * mwords, s);
+  kmask.zero();
+  k_orient_tiles<false><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.n, cnt.p,
+                                                      nullptr, nullptr, ctr.p, bigq.p, ctr.p + 2,
+                                                      kmask.p);
+  TG_CHECK_LAUNCH();
+  k_orient_big<false><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, bigq.p, ctr.p + 2, cnt.p,
+                                              nullptr, nullptr, kmask.p + mwords);
+  TG_CHECK_LAUNCH();
+  TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::InclusiveSum(t, b, cnt.p, out.off.p + 1, (int64_t)g.n, s);
+  });
+  k_orient_tiles<true><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.n, out.off.p,
+                                                     out.desc.p, out.data.p, ctr.p + 1, nullptr,
+                                                     nullptr, kmask.p);
+  TG_CHECK_LAUNCH();
+  k_orient_big<true><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, bigq.p, ctr.p + 2,
+                                             out.off.p, out.desc.p, out.data.p, kmask.p + mwords);
+  TG_CHECK_LAUNCH();
+  g_launches += 6;  // count, big count, scan (init + sweep), fill, big fill
+}
+
+// Gappy single-pass orientation (N_v in the first h_v slots of v's symmetric
+// slot range); kept for comparison with the compact tile kernel.
+void orient_full_gappy(const DevGraph& g, DevEff& out, cudaStream_t s) {
+  TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
+  out.rows = g.n;
+  out.base = 0;
+  out.compact = false;
+  out.entries = g.m2 / 2;
+  if (out.desc.n < (g.n ? g.n : 1)) out.desc.alloc(g.n ? g.n : 1, s);
+  if (out.data.n < (g.m2 ? g.m2 : 1)) out.data.alloc(g.m2 ? g.m2 : 1, s);
+  out.off.release();
+  if (!g.n) return;
+  const uint64_t avg = g.m2 / g.n;
+  if (avg <= 12) launch_orient_gappy<8>(g, out.desc.p, out.data.p, s);
+  else if (avg <= 24) launch_orient_gappy<16>(g, out.desc.p, out.data.p, s);
+  else launch_orient_gappy<32>(g, out.desc.p, out.data.p, s);
+}
+
+void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s) {
+  const uint64_t rows = in.rows;
+  out.rows = rows;
+  out.base = in.base;
+  out.compact = true;
+  out.entries = in.entries;
+  out.off.alloc(rows + 1, s);
+  out.desc.alloc(rows ? rows : 1, s);
+  out.data.alloc(in.entries ? in.entries : 1, s);
+  TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
+  if (!rows) return;
+  DBuf<uint64_t> lens(rows, s);
+  k_desc_lens<<<grid_for(rows, 256), 256, 0, s>>>(in.desc.p, rows, lens.p);
+  TG_CHECK_LAUNCH();
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::InclusiveSum(t, b, lens.p, out.off.p + 1, (int64_t)rows, s);
+  });
+  CsrView v{in.desc.p, in.data.p, in.base};
+  k_gather_compact<<<grid_for(rows * 32, 256, 148u * 32u), 256, 0, s>>>(v, rows, out.off.p, out.data.p);
+  TG_CHECK_LAUNCH();
+  k_desc_from_off<<<grid_for(rows, 256), 256, 0, s>>>(out.off.p, rows, out.desc.p);
+  TG_CHECK_LAUNCH();
+  g_launches += 5;
+}
+
+uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s) {
+  DBuf<unsigned long long> acc(1, s);
+  acc.zero();
+  if (hi > lo) {
+    k_sum_lens<<<grid_for(hi - lo, 256, 148u * 8u), 256, 0, s>>>(e.desc.p, lo - e.base, hi - e.base, acc.p);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
+  }
+  unsigned long long h = 0;
+  TG_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  return h;
 }
 
 // order.hpp:95-104: rank = position in the (degree, id) sort.
@@ -376,14 +773,16 @@ void node_costs_device(const DevGraph& g, const DevEff& eff, int kind, uint64_t*
                        uint64_t* d_prefix, cudaStream_t s) {
   TG_REQUIRE(kind >= TG_COST_N && kind <= TG_COST_NOV, "node_costs: unknown cost kind");
   if (!g.n) return;
+  TG_REQUIRE(eff.base == 0 && eff.rows == g.n, "node_costs needs the full oriented CSR");
+  const CsrView ev{eff.desc.p, eff.data.p, 0};
   if (kind == TG_COST_DPD || kind == TG_COST_NOV) {
     unsigned grid = grid_for(g.n * 32, 256, 148u * 32u);
     if (kind == TG_COST_DPD)
-      k_cost_sum<false><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, eff.off.p, eff.data.p, g.n, d_f);
+      k_cost_sum<false><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, ev, g.n, d_f);
     else
-      k_cost_sum<true><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, eff.off.p, eff.data.p, g.n, d_f);
+      k_cost_sum<true><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, ev, g.n, d_f);
   } else {
-    k_cost_simple<<<grid_for(g.n, 256), 256, 0, s>>>(eff.off.p, g.deg.p, g.n, kind, d_f);
+    k_cost_simple<<<grid_for(g.n, 256), 256, 0, s>>>(eff.desc.p, g.deg.p, g.n, kind, d_f);
   }
   TG_CHECK_LAUNCH();
   ++g_launches;
@@ -410,7 +809,7 @@ uint64_t ordering_cost_device(const DevGraph& g, const DevEff& eff, cudaStream_t
   DBuf<unsigned long long> acc(1, s);
   acc.zero();
   if (g.n) {
-    k_ordering_cost<<<grid_for(g.n, 256, 148u * 8u), 256, 0, s>>>(g.deg.p, eff.off.p, g.n, acc.p);
+    k_ordering_cost<<<grid_for(g.n, 256, 148u * 8u), 256, 0, s>>>(g.deg.p, eff.desc.p, g.n, acc.p);
     TG_CHECK_LAUNCH();
     ++g_launches;
   }

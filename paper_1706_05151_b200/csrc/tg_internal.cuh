@@ -86,18 +86,33 @@ struct DevGraph {
   DBuf<uint32_t> deg;      // n
 };
 
-// Oriented CSR (reference EffectiveAdjacency), possibly partition-local:
-// list(v) = data[off[v-base] .. off[v-base+1]) for v in [base, base+rows).
+// Packed list descriptor: (start << 24) | len.  One 8-byte load gives a
+// list's position and length (len < 2^24, start < 2^40).
+__host__ __device__ __forceinline__ uint64_t desc_start(uint64_t d) { return d >> 24; }
+__host__ __device__ __forceinline__ uint32_t desc_len(uint64_t d) { return (uint32_t)(d & 0xFFFFFFu); }
+__host__ __device__ __forceinline__ uint64_t make_desc(uint64_t start, uint64_t len) {
+  return (start << 24) | len;
+}
+
+// Oriented lists (reference EffectiveAdjacency), possibly partition-local:
+// list(v) = data[start .. start+len) with (start, len) = desc[v-base], for v
+// in [base, base+rows).  Two layouts:
+//  * compact  -- lists back to back (off[] valid, rows+1 entries): partitions
+//    and the exported EffectiveAdjacency;
+//  * gappy    -- N_v in the first h_v slots of v's symmetric-CSR slot range
+//    (start = sym_off[v]); built in ONE pass over the adjacency (the hot path).
 struct DevEff {
   uint64_t rows = 0, entries = 0;
   uint32_t base = 0;
-  DBuf<uint64_t> off;   // rows+1
-  DBuf<uint32_t> data;  // entries
+  bool compact = false;
+  DBuf<uint64_t> desc;  // rows
+  DBuf<uint64_t> off;   // rows+1 (compact layout only)
+  DBuf<uint32_t> data;
 };
 
 // Read-only view passed to kernels.
 struct CsrView {
-  const uint64_t* off;
+  const uint64_t* desc;
   const uint32_t* data;
   uint32_t base;
 };
@@ -106,8 +121,15 @@ struct CsrView {
 void build_graph_device(const uint32_t* d_pairs, uint64_t E, uint64_t n_override,
                         DevGraph& g, cudaStream_t s);
 void compute_degrees(DevGraph& g, cudaStream_t s);
-// Orient rows [vlo, vhi) of g into `out` (out.base = vlo); lists ID-sorted.
+// Orient rows [vlo, vhi) of g into `out` (out.base = vlo), compact layout;
+// lists ID-sorted.
 void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s);
+// Orient the whole graph in one pass, gappy layout (no host sync).
+void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s);
+// Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
+void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
+// sum of list lengths over rows [lo, hi) (host result).
+uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s);
 void degree_rank(const DevGraph& g, uint32_t* d_rank, cudaStream_t s);
 
 // ---- costs / plan (costs.cu) ----
@@ -144,12 +166,15 @@ struct IntersectScratch {
 
 // NodeIteratorN over apex rows [vlo, vhi) of `apex`, N_u from `nu`, middle
 // vertex u restricted to [ulo, uhi).
+// `nu_entries` = size of nu.data (selects 32/64-bit element indexing);
+// `unrestricted` = [ulo, uhi) covers every vertex (no middle-vertex filter).
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
                     uint32_t uhi, const CountOut& out, IntersectScratch& scr,
-                    cudaStream_t s);
+                    cudaStream_t s, uint64_t nu_entries, bool unrestricted);
 // SurrogateCount (engines.hpp:60-76) over received messages.
 void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
-                    const CountOut& out, IntersectScratch& scr, cudaStream_t s);
+                    const CountOut& out, IntersectScratch& scr, cudaStream_t s,
+                    uint64_t nu_entries);
 
 void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,
                        cudaStream_t s);

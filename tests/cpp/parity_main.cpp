@@ -1,0 +1,94 @@
+// C++ drop-in check: the reference's own test cases (test_engines.cpp,
+// test_graph.cpp, test_sequential.cpp) written against the C++ mirror, with
+// only the namespace alias changed.  Built by tests/test_abi.py (g++ against
+// include/ + libtrigraph_b200.so) and run on the GPU by tests/test_gpu_cpp.py.
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "trigraph_b200/trigraph.hpp"
+
+namespace trigraph = trigraph_b200;
+using namespace trigraph;
+
+static int failures = 0;
+#define CHECK(c)                                                   \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      ++failures;                                                  \
+    }                                                              \
+  } while (0)
+
+static Graph g5() { return build_graph({{0, 1}, {0, 2}, {1, 2}, {1, 3}, {2, 3}, {3, 4}}); }
+
+static EngineConfig config(EngineKind e, std::size_t p, CostKind c = CostKind::Dpd) {
+  EngineConfig cfg;
+  cfg.engine = e;
+  cfg.ranks = p;
+  cfg.cost = c;
+  return cfg;
+}
+
+int main(int argc, char** argv) {
+  {  // test_graph.cpp:10-17
+    auto g = build_graph({{0, 1}, {1, 0}, {2, 2}});
+    CHECK(g.num_nodes() == 3);
+    CHECK(g.num_edges() == 1);
+  }
+  {  // test_graph.cpp:57-64
+    auto g = g5();
+    auto ord = compute_order(g);
+    CHECK((ord.rank == std::vector<NodeId>{1, 2, 3, 4, 0}));
+    CHECK(ord.precedes(4, 0));
+    auto eff = effective_adjacency(g);
+    CHECK(eff.total_entries() == 6);
+    CHECK(count_node_iterator_n(g) == 2);
+    CHECK(ordering_cost(g) == 14);
+    CHECK((node_costs(g, CostKind::Dpd).f == std::vector<std::uint64_t>{7, 5, 1, 0, 1}));
+    CHECK((node_costs(g, CostKind::Nov).f == std::vector<std::uint64_t>{0, 4, 6, 4, 0}));
+  }
+  {  // test_engines.cpp:28-64
+    auto g = g5();
+    auto cfg = config(EngineKind::Aop, 2);
+    cfg.boundaries = std::vector<NodeId>{0, 2, 5};
+    auto r = run_engine(g, cfg);
+    CHECK(r.total == 2 && r.per_rank[0].triangles == 2 && r.per_rank[1].triangles == 0);
+    cfg.engine = EngineKind::AnopDirect;
+    r = run_engine(g, cfg);
+    CHECK(r.per_rank[0].data_sent == 3 && r.per_rank[1].data_sent == 3);
+    cfg.engine = EngineKind::AnopSurrogate;
+    r = run_engine(g, cfg);
+    CHECK(r.per_rank[0].triangles == 1 && r.per_rank[1].triangles == 1);
+    CHECK(r.per_rank[0].data_sent == 2 && r.per_rank[1].data_sent == 0);
+  }
+  {  // test_engines.cpp:90-94, 125-139, 172-175
+    std::vector<std::pair<NodeId, NodeId>> k8;
+    for (NodeId u = 0; u < 8; ++u)
+      for (NodeId v = u + 1; v < 8; ++v) k8.push_back({u, v});
+    CHECK(run_engine(build_graph(k8, 8), config(EngineKind::AnopSurrogate, 3, CostKind::Nov)).total == 56);
+    auto cc = clustering_coefficients(g5(), config(EngineKind::Aop, 2));
+    CHECK((cc.triangles_per_node == std::vector<std::uint64_t>{1, 2, 2, 1, 0}));
+    CHECK(cc.coefficient[0] == 1.0 && cc.coefficient[1] == 2.0 / 3.0 && cc.coefficient[4] == 0.0);
+    bool threw = false;
+    try {
+      run_engine(g5(), config(EngineKind::Aop, 0));
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // a PA graph through every engine: totals and per-rank sums agree
+    auto g = gen_pa(20000, 20, 3);
+    std::uint64_t t = count_node_iterator_n(g);
+    for (auto e : {EngineKind::Aop, EngineKind::AnopDirect, EngineKind::AnopSurrogate}) {
+      auto r = run_engine(g, config(e, 8));
+      std::uint64_t s = 0;
+      for (auto& rs : r.per_rank) s += rs.triangles;
+      CHECK(r.total == t && s == t);
+    }
+    std::printf("pa20000 count %llu\n", (unsigned long long)t);
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
+  return failures ? 1 : 0;
+}
