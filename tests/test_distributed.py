@@ -1,0 +1,136 @@
+"""The multi-process path (paper_1706_05151_b200/distributed.py) on CPU:
+world_size 2 and 3 over gloo, with an oracle-backed RankBackend, checked
+against the reference semantics (per-rank T, data_sent, data_recv, plan,
+total) of the oracle's run_engine.  The GPU backend runs the same driver on
+the B200 box (tests/test_gpu_distributed.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import binding as O
+from paper_1706_05151_b200 import distributed as D
+from paper_1706_05151_b200.trigraph import CostKind, EngineKind
+
+COSTNAME = {CostKind.N: "N", CostKind.Dpd: "DPD", CostKind.Nov: "NOV"}
+
+
+class OracleRankBackend(D.RankBackend):
+    """Per-rank compute restated on the oracle's CSR (test infrastructure)."""
+
+    def __init__(self, g: O.CSR):
+        self.g = g
+        self.device = torch.device("cpu")
+        self.eoff, self.eff = O.effective(g)
+
+    def lst(self, v):
+        return self.eff[self.eoff[v]:self.eoff[v + 1]]
+
+    def plan(self, cost, p):
+        f, _ = O.node_costs(self.g, COSTNAME[cost])
+        return O.compute_boundaries(f, p)
+
+    def aop_count(self, b, rank):
+        t = 0
+        for v in range(int(b[rank]), int(b[rank + 1])):
+            nv = self.lst(v)
+            for u in nv:
+                t += len(np.intersect1d(nv, self.lst(u), assume_unique=True))
+        return t
+
+    def pack(self, b, rank):
+        p = len(b) - 1
+        inner = b[1:-1]
+        per = [[] for _ in range(p)]
+        for v in range(int(b[rank]), int(b[rank + 1])):
+            nv = self.lst(v)
+            owners = np.searchsorted(inner, nv, side="right")
+            for j in sorted(set(int(o) for o in owners) - {rank}):
+                per[j].append(v)
+        msgs = np.array([len(x) for x in per], np.uint64)
+        words = np.array([sum(len(self.lst(v)) for v in x) for x in per], np.uint64)
+        hdr, dat = [], []
+        for j in range(p):
+            for v in per[j]:
+                hdr += [v, len(self.lst(v))]
+                dat += list(self.lst(v))
+        return (msgs, words, torch.tensor(hdr, dtype=torch.int32),
+                torch.tensor(dat, dtype=torch.int32))
+
+    def surrogate_count(self, b, rank, hdr, nmsgs, data):
+        cb, ce = int(b[rank]), int(b[rank + 1])
+        t = 0
+        for v in range(cb, ce):  # local intersections (u in core)
+            nv = self.lst(v)
+            for u in nv[(nv >= cb) & (nv < ce)]:
+                t += len(np.intersect1d(nv, self.lst(u), assume_unique=True))
+        h = hdr.numpy().reshape(-1, 2)
+        d = data.numpy().astype(np.uint32)
+        o = 0
+        for k in range(nmsgs):  # SurrogateCount on received lists
+            x = d[o:o + h[k, 1]]
+            o += h[k, 1]
+            for u in x[(x >= cb) & (x < ce)]:
+                t += len(np.intersect1d(self.lst(u), x, assume_unique=True))
+        return t
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for (n, dens, seed, engine, cost) in cases:
+            g = O.random_graph(n, dens, seed)
+            rep = D.run_engine_distributed(OracleRankBackend(g), engine, cost)
+            out.append((rep.total, rep.boundaries.tolist(),
+                        [(r.triangles, r.data_sent, r.data_recv) for r in rep.per_rank]))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_engines_match_reference_semantics(world):
+    cases = []
+    rng = np.random.default_rng(world)
+    for i in range(3):
+        n = int(rng.integers(25, 60))
+        dens = float(rng.uniform(0.15, 0.5))
+        seed = int(rng.integers(1 << 60))
+        for engine in (EngineKind.Aop, EngineKind.AnopSurrogate):
+            for cost in (CostKind.N, CostKind.Dpd, CostKind.Nov):
+                cases.append((n, dens, seed, engine, cost))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for k, (n, dens, seed, engine, cost) in enumerate(cases):
+        g = O.random_graph(n, dens, seed)
+        name = "aop" if engine == EngineKind.Aop else "anop-surrogate"
+        want = O.run_engine(g, name, world, COSTNAME[cost])
+        for r in range(world):  # every rank returns the same report
+            total, b, per = results[r][k]
+            assert total == want.total
+            assert b == want.boundaries.tolist()
+            assert [x[0] for x in per] == want.triangles.tolist()
+            assert [x[1] for x in per] == want.data_sent.tolist()
+            assert [x[2] for x in per] == want.data_recv.tolist()

@@ -1,0 +1,38 @@
+"""The distributed driver's CUDA backend on the B200 box.  One GPU is
+available, so the NCCL group has one rank (ranks that wait on each other must
+not share a GPU); the multi-rank exchange logic is covered with gloo in
+tests/test_distributed.py and the per-rank device entries with p = 3
+emulated ranks in tests/test_gpu_parity.py::test_device_step_and_rank_entries."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+
+from oracle import binding as O
+from paper_1706_05151_b200 import distributed as D
+from paper_1706_05151_b200 import trigraph as T
+
+pytestmark = pytest.mark.gpu
+
+
+def test_nccl_single_rank_driver():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        pairs = T.gen_pa(30000, 20, 5)
+        ref = O.build_graph(pairs)
+        want = O.count(ref)[0]
+        g = T.build_graph(pairs)
+        be = D.CudaRankBackend(g)
+        for engine in (T.EngineKind.Aop, T.EngineKind.AnopSurrogate):
+            rep = D.run_engine_distributed(be, engine, T.CostKind.Dpd)
+            assert rep.total == want
+            assert rep.per_rank[0].triangles == want and rep.per_rank[0].data_sent == 0
+    finally:
+        dist.destroy_process_group()
