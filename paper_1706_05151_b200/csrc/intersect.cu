@@ -7,14 +7,15 @@
 // (sequential.hpp:36-46) / RankSink (engines.hpp:303-321).
 //
 // B200 design (integer set intersection; no tensor cores):
-//  * apex-centric: one warp (short N_v) or one 512-thread CTA (long N_v) owns
-//    apex v and stages N_v in shared memory once, so N_v is read from HBM once
-//    per apex instead of once per oriented edge;
+//  * apex-centric: one warp (h_v <= 64) or one 512-thread CTA (longer N_v)
+//    owns apex v and stages N_v in shared memory once (an 8192-bit filter +
+//    sorted copy for the warp path, an exact hash table for the CTA path), so
+//    N_v is read from HBM once per apex instead of once per oriented edge;
 //  * the work of the apex, sum_{u in N_v} h_u elements, is flattened across
-//    the lanes: each lane takes one element x of one N_u (coalesced reads of
-//    consecutive N_u entries), finds its u by a 5-step search over the
-//    prefix of list lengths, and tests x ∈ N_v by binary search in shared
-//    memory.  A triangle (v,u,x) is found exactly once (Theorem 1).
+//    the lanes: each lane takes one element x of one N_u (consecutive lanes
+//    read consecutive entries of the same list), finds its u from a bit table
+//    of segment starts, and tests x ∈ N_v in shared memory.  A triangle
+//    (v,u,x) is found exactly once (Theorem 1).
 //  * counts are reduced with __ballot_sync/__popc and one 64-bit atomic per
 //    warp per kernel; per-node tallies fold T_v per apex and T_u per edge
 //    before touching global atomics; listing compacts found triples with one
@@ -29,8 +30,6 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;  // warp path: 256 threads
 constexpr int kWCap = 64;          // apex lists up to 64 entries on the warp path
-constexpr int kBT = 512;           // CTA path threads
-constexpr int kBCap = 12288;       // CTA path: N_v entries staged in smem (48 KB)
 
 struct RowsApex {
   CsrView view;
@@ -70,17 +69,6 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
 __device__ __forceinline__ bool contains_u32(const uint32_t* a, uint32_t n, uint32_t x) {
   uint32_t i = lower_bound_u32(a, n, x);
   return i < n && a[i] == x;
-}
-
-// largest j in [0, nb) with start[j] <= idx (start[0] == 0, nondecreasing)
-__device__ __forceinline__ int seg_of(const uint32_t* start, int nb, uint32_t idx) {
-  int lo = 0, hi = nb - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (start[mid] <= idx) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
 }
 
 __device__ __forceinline__ void emit_triple(const CountOut& out, unsigned long long pos, uint32_t a,
@@ -290,100 +278,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 
 // ------------------------------------------------------------- CTA path
 
-template <bool TALLY, bool LIST, class Apex>
-__global__ void __launch_bounds__(kBT, 2)
-k_intersect_block(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
-                  const uint32_t* __restrict__ big, const unsigned long long* __restrict__ big_count,
-                  uint64_t big_cap, uint32_t bcap) {
-  extern __shared__ uint32_t sNvDyn[];
-  using Scan = cub::BlockScan<uint32_t, kBT>;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t sStart[kBT];
-  __shared__ uint64_t sLo[kBT];
-  __shared__ uint32_t sU[kBT];
-  __shared__ unsigned sCntU[kBT];
-  __shared__ uint32_t sJ[2];
-  __shared__ uint32_t sTotal;
-  __shared__ unsigned long long sApex;
-  const unsigned t = threadIdx.x, lane = t & 31;
-  const unsigned FULL = 0xffffffffu;
-  uint64_t nbig = *big_count;
-  if (nbig > big_cap) nbig = big_cap;
-  unsigned long long acc = 0;
-
-  for (uint64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
-    uint32_t v, hv;
-    const uint32_t* L;
-    A.get(big[bi], v, L, hv);
-    const bool in_smem = hv <= bcap;
-    const uint32_t* Nv = in_smem ? sNvDyn : L;
-    if (in_smem)
-      for (uint32_t i = t; i < hv; i += kBT) sNvDyn[i] = L[i];
-    if (t == 0) sApex = 0;
-    __syncthreads();
-    if (t == 0) {
-      sJ[0] = lower_bound_u32(Nv, hv, ulo);
-      sJ[1] = lower_bound_u32(Nv, hv, uhi);
-    }
-    __syncthreads();
-    const uint32_t jlo = sJ[0], jhi = sJ[1];
-    unsigned long long apex_cnt = 0;
-    for (uint32_t jb = jlo; jb < jhi; jb += kBT) {
-      const int nb = (int)min((uint32_t)kBT, jhi - jb);
-      uint32_t len = 0, u = 0;
-      uint64_t lo = 0;
-      if ((int)t < nb) {
-        u = Nv[jb + t];
-        const uint64_t d = nu.desc[u - nu.base];
-        lo = desc_start(d);
-        len = desc_len(d);
-      }
-      uint32_t excl, S;
-      Scan(scan_tmp).ExclusiveSum(len, excl, S);
-      sStart[t] = excl;
-      sLo[t] = lo;
-      if (TALLY || LIST) sU[t] = u;
-      if (TALLY) sCntU[t] = 0;
-      __syncthreads();
-      for (uint32_t base = 0; base < S; base += kBT) {
-        const uint32_t idx = base + t;
-        bool found = false;
-        int jj = 0;
-        uint32_t x = 0;
-        if (idx < S) {
-          jj = seg_of(sStart, nb, idx);
-          x = nu.data[sLo[jj] + (idx - sStart[jj])];
-          found = contains_u32(Nv, hv, x);
-        }
-        const unsigned m = __ballot_sync(FULL, found);
-        apex_cnt += __popc(m);  // per-warp partial, summed below
-        if (TALLY && found) {
-          atomicAdd(&out.tally[x], 1ull);
-          atomicAdd(&sCntU[jj], 1u);
-        }
-        if (LIST && m) {
-          unsigned long long b0 = 0;
-          if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
-          b0 = __shfl_sync(FULL, b0, 0);
-          if (found) emit_triple(out, b0 + __popc(m & ((1u << lane) - 1u)), v, sU[jj], x);
-        }
-      }
-      __syncthreads();
-      if (TALLY && (int)t < nb && sCntU[t])
-        atomicAdd(&out.tally[sU[t]], (unsigned long long)sCntU[t]);
-      __syncthreads();
-    }
-    // apex_cnt is replicated across the lanes of each warp
-    if (lane == 0 && apex_cnt) atomicAdd(&sApex, apex_cnt);
-    __syncthreads();
-    if (t == 0) {
-      if (TALLY && sApex) atomicAdd(&out.tally[v], sApex);
-      acc += sApex;
-    }
-    __syncthreads();
-  }
-  if (t == 0 && acc) atomicAdd(out.total, acc);
-}
+#include "cta.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
@@ -395,13 +290,33 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   ++g_launches;
 }
 
+// CTA-path hash table: 2^14 slots (64 KB) holds N_v up to 4096 entries at load
+// factor 1/4; g_block_cap (tests) lowers it to exercise the global fallback.
+template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
+void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const CountOut& out,
+                IntersectScratch& scr, cudaStream_t s) {
+  uint32_t tl2 = 14;
+  if (g_block_cap) {
+    tl2 = 5;
+    while ((1u << tl2) < 4u * g_block_cap) ++tl2;
+  }
+  const int dyn = (int)((1u << tl2) * 4);
+  TG_CUDA(cudaFuncSetAttribute(k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex><<<148 * 2, kCT, dyn, s>>>(
+      A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, tl2, scr.big_count.p + 1);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
 template <bool TALLY, bool LIST, class Apex>
 void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
                  const CountOut& out, IntersectScratch& scr, cudaStream_t s, bool filter,
                  bool wide) {
   if (!items) return;
   scr.ensure(items, s);
-  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, sizeof(unsigned long long), s));
+  // [0]: long-apex queue size, [1]: CTA work counter
+  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, 2 * sizeof(unsigned long long), s));
   if (filter) {
     if (wide) launch_warp<TALLY, LIST, true, true>(A, items, nu, ulo, uhi, out, scr, s);
     else launch_warp<TALLY, LIST, true, false>(A, items, nu, ulo, uhi, out, scr, s);
@@ -409,14 +324,13 @@ void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
     if (wide) launch_warp<TALLY, LIST, false, true>(A, items, nu, ulo, uhi, out, scr, s);
     else launch_warp<TALLY, LIST, false, false>(A, items, nu, ulo, uhi, out, scr, s);
   }
-  const uint32_t bcap = g_block_cap ? g_block_cap : (uint32_t)kBCap;
-  const int dyn = (int)(bcap * 4);
-  TG_CUDA(cudaFuncSetAttribute(k_intersect_block<TALLY, LIST, Apex>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-  k_intersect_block<TALLY, LIST, Apex><<<148 * 2, kBT, dyn, s>>>(
-      A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, bcap);
-  TG_CHECK_LAUNCH();
-  ++g_launches;
+  if (filter) {
+    if (wide) launch_cta<TALLY, LIST, true, true>(A, nu, ulo, uhi, out, scr, s);
+    else launch_cta<TALLY, LIST, true, false>(A, nu, ulo, uhi, out, scr, s);
+  } else {
+    if (wide) launch_cta<TALLY, LIST, false, true>(A, nu, ulo, uhi, out, scr, s);
+    else launch_cta<TALLY, LIST, false, false>(A, nu, ulo, uhi, out, scr, s);
+  }
 }
 
 template <class Apex>
@@ -449,7 +363,7 @@ uint32_t g_block_cap = 0;
 
 void IntersectScratch::ensure(uint64_t cap, cudaStream_t s) {
   if (big.n < cap) big.alloc(cap, s);
-  if (!big_count.n) big_count.alloc(1, s);
+  if (big_count.n < 2) big_count.alloc(2, s);
 }
 
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,

@@ -1,0 +1,105 @@
+#!/usr/bin/env python
+"""Run BASELINE.json's configs on one GPU: generate, build, orient + count,
+time (CUDA events), cross-check engines.  Usage:
+    python tools/run_configs.py C1 C3 C4 [--small]
+Prints one JSON line per config."""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1706_05151_b200 import trigraph as T  # noqa: E402
+from paper_1706_05151_b200._lib import check, lib  # noqa: E402
+
+CONFIGS = {
+    "C1": ("gnm", dict(n=100_000, m=1_000_000, seed=1)),
+    "C2": ("pa", dict(n=10_000_000, d=40, seed=7)),
+    "C3": ("rmat", dict(scale=24, ef=16, seed=1)),
+    "C4": ("ws", dict(n=50_000_000, k=20, beta=0.1, seed=1)),
+    "C5": ("pa", dict(n=100_000_000, d=40, seed=7)),
+}
+SMALL = {"C1": dict(n=100_000, m=1_000_000), "C2": dict(n=200_000), "C3": dict(scale=18),
+         "C4": dict(n=1_000_000), "C5": dict(n=1_000_000)}
+
+
+def gen(kind, p):
+    if kind == "gnm":
+        return T.gen_gnm(p["n"], p["m"], p["seed"]), p["n"]
+    if kind == "pa":
+        return T.gen_pa(p["n"], p["d"], p["seed"]), p["n"]
+    if kind == "rmat":
+        return T.gen_rmat(p["scale"], p["ef"], 0.57, 0.19, 0.19, p["seed"]), 1 << p["scale"]
+    if kind == "ws":
+        return T.gen_ws(p["n"], p["k"], p["beta"], p["seed"]), p["n"]
+    raise ValueError(kind)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--small", action="store_true")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--engines", action="store_true")
+    a = ap.parse_args()
+    L = lib()
+    for name in a.configs:
+        kind, p = CONFIGS[name]
+        p = dict(p)
+        if a.small:
+            p.update(SMALL[name])
+        t0 = time.time()
+        pairs, n = gen(kind, p)
+        t1 = time.time()
+        g = T.build_graph(pairs, n)
+        del pairs
+        torch.cuda.synchronize()
+        t2 = time.time()
+        m = g.num_edges()
+        W = T.ordering_cost(g)
+        s = torch.cuda.Stream()
+        torch.cuda.set_stream(s)
+        check(L.tg_set_stream(g._h, C.c_void_p(s.cuda_stream)))
+        d = torch.zeros(1, dtype=torch.int64, device="cuda")
+        dp = C.c_void_p(d.data_ptr())
+        for _ in range(2):
+            check(L.tg_orient_device(g._h))
+            check(L.tg_count_device(g._h, dp))
+        torch.cuda.synchronize()
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(3 * a.steps)]
+        for i in range(a.steps):
+            es[3 * i].record(s)
+            check(L.tg_orient_device(g._h))
+            es[3 * i + 1].record(s)
+            check(L.tg_count_device(g._h, dp))
+            es[3 * i + 2].record(s)
+        torch.cuda.synchronize()
+        orient = sum(es[3 * i].elapsed_time(es[3 * i + 1]) for i in range(a.steps)) / a.steps
+        isect = sum(es[3 * i + 1].elapsed_time(es[3 * i + 2]) for i in range(a.steps)) / a.steps
+        tri = int(d.item())
+        rec = {"config": name, "params": p, "n": n, "m": m, "W": W, "triangles": tri,
+               "gen_s": round(t1 - t0, 2), "build_s": round(t2 - t1, 2),
+               "orient_ms": orient, "intersect_ms": isect,
+               "edges_per_s": m / ((orient + isect) / 1e3),
+               "hbm_frac_4W": 4 * W / (isect / 1e3) / 6534.5e9}
+        if a.engines:
+            for eng, pr in ((T.EngineKind.Aop, 8), (T.EngineKind.AnopSurrogate, 8)):
+                torch.cuda.synchronize()
+                t = time.time()
+                rep = T.run_engine(g, T.EngineConfig(engine=eng, ranks=pr))
+                rec[f"{T.to_string(eng)}_total"] = rep.total
+                rec[f"{T.to_string(eng)}_s"] = round(time.time() - t, 3)
+                assert rep.total == tri, (eng, rep.total, tri)
+        print(json.dumps(rec), flush=True)
+        g.close()
+        torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
