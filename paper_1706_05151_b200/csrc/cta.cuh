@@ -1,11 +1,11 @@
 // cta.cuh -- CTA path of the intersection (apexes with h_v > kWCap), included
 // by intersect.cu inside namespace tgb::{anon}.
 //
-// One 512-thread CTA per long apex (claimed dynamically; skewed graphs such
-// as R-MAT have apexes with h_v in the thousands and sum_{u in N_v} h_u in
-// the millions).  N_v is inserted into a shared-memory open-addressing hash
-// table at load factor <= 1/4 (linear probing, ~1.4 probes per miss), so
-// membership is exact without a sorted-array search.  The apex's items are
+// One 512-thread CTA per long or heavy apex (claimed dynamically; skewed
+// graphs such as R-MAT have apexes with h_v in the thousands and
+// sum_{u in N_v} h_u in the millions).  N_v is inserted into the two-choice
+// bucketed hash set Ht4 in shared memory (<= 1 key per 4-slot bucket), so
+// membership is two LDS.128 without a sorted-array search.  The apex's items are
 // processed per 512-u batch in windows of 32K items: a window-wide bit table
 // of segment starts plus per-word prefix counts give every lane its middle
 // vertex u with two broadcast LDS and two POPC; each warp streams 32-item
@@ -16,11 +16,7 @@ constexpr int kCT = 512;
 constexpr int kCWarps = kCT / 32;
 constexpr int kCTbl = 1024;      // table words per window: 32768 items
 constexpr int kCUnroll = 4;
-constexpr uint32_t kCEmpty = 0xffffffffu;
-
-__device__ __forceinline__ uint32_t ht_hash(uint32_t x, uint32_t shift) {
-  return (x * 0x9E3779B1u) >> shift;
-}
+constexpr uint32_t kCEmpty = 0xffffffffu;  // == kNoItem
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 __global__ void __launch_bounds__(kCT, 2)
@@ -29,7 +25,7 @@ k_intersect_cta(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                 uint64_t big_cap, uint32_t tcap_log2, unsigned long long* __restrict__ work_ctr) {
   using Adj = typename std::conditional<WIDE, long long, uint32_t>::type;
   using Scan = cub::BlockScan<uint32_t, kCT>;
-  extern __shared__ uint32_t sHt[];  // hash table, 2^tcap_log2 slots
+  extern __shared__ __align__(16) uint32_t sHt[];  // hash table, 2^tcap_log2 slots
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ Adj sAdj[kCT];
   __shared__ uint32_t sSt[kCT];
@@ -39,6 +35,7 @@ k_intersect_cta(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   __shared__ uint32_t sPre[kCTbl];
   __shared__ uint32_t sJ[2];
   __shared__ unsigned long long sItem, sApex;
+  __shared__ int sOvf;
   const unsigned t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
@@ -55,19 +52,28 @@ k_intersect_cta(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
     uint32_t v, hv;
     const uint32_t* L;
     A.get(big[bi], v, L, hv);
-    // table of N_v at load factor <= 1/4 when it fits, else global search
-    const bool in_ht = 4ull * hv <= tcap;
-    uint32_t tl2 = 5;
-    while ((1u << tl2) < 4u * hv && tl2 < tcap_log2) ++tl2;
-    const uint32_t tsize = 1u << tl2, tshift = 32 - tl2, tmask = tsize - 1;
-    if (in_ht) {
-      for (uint32_t i = t; i < tsize; i += kCT) sHt[i] = kCEmpty;
-      __syncthreads();
-      for (uint32_t i = t; i < hv; i += kCT) {
-        const uint32_t x = L[i];
-        uint32_t s = ht_hash(x, tshift);
-        while (atomicCAS(&sHt[s], kCEmpty, x) != kCEmpty) s = (s + 1) & tmask;
-      }
+    // two-choice bucketed table of N_v (<= 1 key per 4-slot bucket on
+    // average) when it fits, else binary search of the sorted list in HBM
+    uint32_t bits = 3;
+    while ((1u << bits) < hv) ++bits;
+    bool in_ht = (4u << bits) <= tcap;
+    const Ht4 H{sHt, 32u - bits};
+    // filter in front of the table: 16 bits per key (>= 1024 bits)
+    uint32_t bmb = bits + 4;
+    if (bmb < 10) bmb = 10;
+    if ((1u << (bmb - 5)) > tcap / 8) bmb = 5 + 31 - __clz(tcap / 8);
+    uint32_t* Bm = sHt + tcap;
+    const uint32_t bshift = 32 - bmb, bwords = 1u << (bmb - 5);
+    if (t == 0) sOvf = 0;
+    for (uint32_t i = t; i < bwords; i += kCT) Bm[i] = 0;
+    if (in_ht)
+      for (uint32_t i = t; i < (4u << bits); i += kCT) sHt[i] = kCEmpty;
+    __syncthreads();
+    for (uint32_t i = t; i < hv; i += kCT) {
+      const uint32_t x = L[i];
+      if (in_ht && !H.insert(x)) sOvf = 1;
+      const uint32_t h = (x * 0x2545F491u) >> bshift;
+      atomicOr(&Bm[h >> 5], 1u << (h & 31));
     }
     if (t == 0) {
       sApex = 0;
@@ -75,6 +81,7 @@ k_intersect_cta(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       sJ[1] = FILTER ? lower_bound_u32(L, hv, uhi) : hv;
     }
     __syncthreads();
+    if (sOvf) in_ht = false;  // an insertion found both buckets full
     const uint32_t jlo = sJ[0], jhi = sJ[1];
     unsigned long long apex_cnt = 0;
     for (uint32_t jb = jlo; jb < jhi; jb += kCT) {
@@ -139,20 +146,11 @@ k_intersect_cta(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #pragma unroll
           for (int q = 0; q < kCUnroll; ++q) {
             const uint32_t x = xs[q];
-            bool found = false;
-            if (x != kNoItem) {
-              if (in_ht) {
-                uint32_t s = ht_hash(x, tshift);
-                for (;;) {
-                  const uint32_t k = sHt[s];
-                  if (k == x) { found = true; break; }
-                  if (k == kCEmpty) break;
-                  s = (s + 1) & tmask;
-                }
-              } else {
-                found = contains_u32(L, hv, x);
-              }
-            }
+            const uint32_t h = (x * 0x2545F491u) >> bshift;
+            const bool hit = x != kNoItem && ((Bm[h >> 5] >> (h & 31)) & 1u);
+            if (!__any_sync(FULL, hit)) continue;
+            bool found = false;  // exact check of filter hits only
+            if (hit) found = in_ht ? H.contains(x) : contains_u32(L, hv, x);
             const unsigned m = __ballot_sync(FULL, found);
             if (m) {
               apex_cnt += __popc(m);

@@ -88,12 +88,7 @@ __device__ __forceinline__ void emit_triple(const CountOut& out, unsigned long l
 // ------------------------------------------------------------- warp path
 
 constexpr int kBmWords = 256;   // per-warp membership filter: 8192 bits
-constexpr int kTblWords = 32;   // segment-start table window: 1024 items
-constexpr int kUnroll = 4;      // chunks (of 32 items) in flight per warp
-// Sentinel for "no item": 0xffffffff is never a NodeId of an n < 2^32 graph.
-constexpr uint32_t kNoItem = 0xffffffffu;
-
-__device__ __forceinline__ uint32_t bm_hash(uint32_t x) { return (x * 0x9E3779B1u) >> 19; }
+__device__ __forceinline__ uint32_t bm_hash(uint32_t x) { return (x * 0x2545F491u) >> 19; }
 
 // Branch-free membership in an ascending shared-memory array of n <= 64.
 __device__ __forceinline__ bool contains_small(const uint32_t* a, uint32_t n, uint32_t x) {
@@ -103,19 +98,66 @@ __device__ __forceinline__ bool contains_small(const uint32_t* a, uint32_t n, ui
     if (pos + step <= n && a[pos + step - 1] < x) pos += step;
   return pos < n && a[pos] == x;
 }
+constexpr int kTblWords = 32;   // segment-start table window: 1024 items
+constexpr int kUnroll = 4;      // chunks (of 32 items) in flight per warp
+constexpr uint32_t kWarpWork = 4096;  // items of the first u-batch above which
+                                      // an apex moves to the CTA path
+// Sentinel for "no item" / "empty slot": 0xffffffff is never a NodeId of an
+// n < 2^32 graph.
+constexpr uint32_t kNoItem = 0xffffffffu;
+
+// Two-choice bucketed hash set of N_v in shared memory: 2^b buckets of 4
+// slots (16 B).  A key lives in the less loaded of its two buckets, so a
+// lookup is two LDS.128 and eight compares -- exact, branch-free, the same
+// cost for members and non-members.  With <= 1 key per bucket on average the
+// max load stays ~2-3; an insertion that finds both buckets full sets
+// `overflow` and the apex falls back to searching the sorted list.
+struct Ht4 {
+  uint32_t* slots;  // 4 * 2^bits words, 16-byte aligned, kNoItem = empty
+  uint32_t shift;   // 32 - bits
+  __device__ __forceinline__ uint32_t b1(uint32_t x) const { return (x * 0x9E3779B1u) >> shift; }
+  __device__ __forceinline__ uint32_t b2(uint32_t x) const {
+    return ((x ^ 0x5BD1E995u) * 0x85EBCA6Bu) >> shift;
+  }
+  // x == kNoItem (an idle lane) matches empty slots, so it is excluded
+  __device__ __forceinline__ bool contains(uint32_t x) const {
+    const uint4 a = *reinterpret_cast<const uint4*>(slots + 4 * b1(x));
+    const uint4 c = *reinterpret_cast<const uint4*>(slots + 4 * b2(x));
+    return ((a.x == x) | (a.y == x) | (a.z == x) | (a.w == x) | (c.x == x) | (c.y == x) |
+            (c.z == x) | (c.w == x)) &
+           (x != kNoItem);
+  }
+  // concurrent insertion (atomicCAS); false when both buckets are full
+  __device__ __forceinline__ bool insert(uint32_t x) const {
+    const uint32_t ba = b1(x), bb = b2(x);
+    const volatile uint32_t* vs = slots;
+    for (;;) {
+      int la = 0, lc = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        la += vs[4 * ba + i] != kNoItem;
+        lc += vs[4 * bb + i] != kNoItem;
+      }
+      if (la == 4 && lc == 4) return false;
+      const uint32_t bk = (la <= lc) ? ba : bb;
+      const int l = (la <= lc) ? la : lc;
+      if (atomicCAS(slots + 4 * bk + l, kNoItem, x) == kNoItem) return true;
+    }
+  }
+};
 
 // One warp per apex v (h_v <= kWCap).
-//  * N_v is staged in shared memory together with an 8192-bit hashed filter.
+//  * N_v is staged in shared memory, ID-sorted, with an 8192-bit hashed
+//    filter.
 //  * The apex's work, sum_{u in N_v} h_u elements, is flattened over the
 //    lanes in 32-item chunks; kUnroll chunks are loaded before any is used.
 //  * A lane finds the segment (middle vertex u) of its item from a per-window
 //    bit table of segment starts: jj = #starts <= item - 1 (one broadcast LDS,
 //    two POPCs), then fetches its element x of N_u (consecutive lanes read
 //    consecutive addresses of the same list).
-//  * x is rejected by one filter probe; only when some lane of the warp hits
-//    (true members + ~0.3% false positives per lane) does the warp take the
-//    rare path: a branch-free 6-step search of N_v confirms, and __ballot /
-//    __popc count the triangles.
+//  * x is rejected by one filter probe (one LDS.32 per lane); only chunks in
+//    which some lane hits (members + ~0.3% false positives) run the exact
+//    branch-free 6-step search of N_v; __ballot / __popc count the triangles.
 // FILTER restricts the middle vertex to [ulo, uhi) (SurrogateCount's core
 // range); WIDE selects 64-bit element indexing (> 2^32 list entries).
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
@@ -138,10 +180,10 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   const uint64_t nitems = A.count();
   uint32_t* Nv = sNv[w];
   uint32_t* Bm = sBm[w];
-  uint32_t* Tbl = sTbl[w];
-  unsigned long long acc = 0;
 #pragma unroll
   for (int i = 0; i < kBmWords / 32; ++i) Bm[lane + 32 * i] = 0;
+  uint32_t* Tbl = sTbl[w];
+  unsigned long long acc = 0;
   __syncwarp();
 
   for (uint64_t k = (uint64_t)blockIdx.x * kWarpsPerBlock + w; k < nitems;
@@ -193,6 +235,15 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         if ((int)lane >= o) incl += t;
       }
       const uint32_t S = __shfl_sync(FULL, incl, 31);
+      if (jb == jlo && S > kWarpWork) {
+        // heavy apex (short N_v but hub neighbours, e.g. R-MAT): hand the
+        // whole apex to the CTA path so one warp cannot become a straggler
+        if (lane == 0) {
+          unsigned long long pos = atomicAdd(big_count, 1ull);
+          if (pos < big_cap) big[pos] = (uint32_t)k;
+        }
+        break;
+      }
       if (S == 0) continue;
       // compact the non-empty segments: segment c lives in lane c
       const unsigned ne = __ballot_sync(FULL, len > 0);
@@ -231,21 +282,26 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             if (WIDE) xs[q] = idx < S ? __ldg(nu.data + ((long long)a + idx)) : kNoItem;
             else xs[q] = idx < S ? __ldg(nu.data + (uint32_t)((uint32_t)a + idx)) : kNoItem;
           }
-          // branch-free filter probes, one vote for all kUnroll chunks
+          // filter: one conflict-light LDS.32 per item
           unsigned hits = 0;
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
             const uint32_t h = bm_hash(xs[q]);
-            const unsigned bit = (Bm[h >> 5] >> (h & 31)) & (unsigned)(xs[q] != kNoItem);
-            hits |= bit << q;
+            hits |= ((Bm[h >> 5] >> (h & 31)) & (unsigned)(xs[q] != kNoItem)) << q;
           }
           if (!__any_sync(FULL, hits != 0)) continue;
+          // exact check of filter hits only: branch-free 6-step search of the
+          // sorted N_v (cheaper than a bucket probe at PA/WS list lengths)
+          unsigned fnd = 0;
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q)
+            if ((hits >> q) & 1u) fnd |= (unsigned)contains_small(Nv, hv, xs[q]) << q;
+          if (!__any_sync(FULL, fnd != 0)) continue;
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
             const uint32_t x = xs[q];
-            const bool hit = (hits >> q) & 1u;
-            if (__any_sync(FULL, hit)) {  // rare: confirm against N_v
-              const bool found = hit && contains_small(Nv, hv, x);
+            const bool found = (fnd >> q) & 1u;
+            {
               const unsigned m = __ballot_sync(FULL, found);
               apex_cnt += __popc(m);
               if (TALLY && found) {
@@ -269,7 +325,8 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
     }
     if (TALLY && lane == 0 && apex_cnt) atomicAdd(&out.tally[v], (unsigned long long)apex_cnt);
     acc += apex_cnt;
-    // clear the filter words this apex touched
+    // clear the filter words this apex set
+    __syncwarp();
     for (uint32_t i = lane; i < hv; i += 32) Bm[bm_hash(Nv[i]) >> 5] = 0;
     __syncwarp();
   }
@@ -300,7 +357,7 @@ void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const Cou
     tl2 = 5;
     while ((1u << tl2) < 4u * g_block_cap) ++tl2;
   }
-  const int dyn = (int)((1u << tl2) * 4);
+  const int dyn = (int)((1u << tl2) * 4 + (1u << tl2) / 2);  // table + filter (tcap/8 words)
   TG_CUDA(cudaFuncSetAttribute(k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
   k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex><<<148 * 2, kCT, dyn, s>>>(
