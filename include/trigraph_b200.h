@@ -181,6 +181,10 @@ uint64_t tg_kernel_launches(void);
 /* Test hook: shared-memory capacity (entries) of the CTA-path apex staging;
  * lists longer than this are searched in global memory.  0 = default. */
 void tg_debug_set_block_cap(uint32_t entries);
+/* Test hook: warp-path kernel, 0 = automatic (apex groups when the mean
+ * oriented list is <= 16 entries, else one apex per warp iteration), 1 = one
+ * apex per warp iteration, 2 = apex groups.  All exact. */
+void tg_debug_set_warp_variant(int32_t variant);
 /* Device-side time (ms) of the last intersection pass (CUDA events on the
  * launching stream); 0 if none. */
 double tg_last_intersect_ms(tg_graph* g);

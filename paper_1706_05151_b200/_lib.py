@@ -71,6 +71,7 @@ SIGNATURES = {
     "tg_kernel_launches": (_u64, []),
     "tg_last_intersect_ms": (_dbl, [_vp]),
     "tg_debug_set_block_cap": (None, [_u32]),
+    "tg_debug_set_warp_variant": (None, [_i32]),
     "tg_gen_pa": (_i32, [_u64, _u64, _u64, _pvp, _pu64]),
     "tg_gen_gnp": (_i32, [_u64, _dbl, _u64, _pvp, _pu64]),
     "tg_gen_gnm": (_i32, [_u64, _u64, _u64, _pvp, _pu64]),

@@ -71,7 +71,9 @@ using tgb::CsrView;
 using tgb::DBuf;
 using tgb::DevEff;
 
-CsrView view(const DevEff& e) { return CsrView{e.desc.p, e.data.p, e.base}; }
+CsrView view(const DevEff& e) {
+  return CsrView{e.desc.p, e.data.p, e.base, e.rows ? (float)e.entries / (float)e.rows : 0.f};
+}
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
@@ -343,6 +345,8 @@ const char* tg_status_string(tg_status s) {
 uint64_t tg_kernel_launches(void) { return tgb::g_launches; }
 
 void tg_debug_set_block_cap(uint32_t entries) { tgb::g_block_cap = entries; }
+
+void tg_debug_set_warp_variant(int32_t variant) { tgb::g_warp_variant = variant; }
 
 tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pairs,
                               uint64_t n_override, tg_graph** out) {

@@ -336,13 +336,27 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 // ------------------------------------------------------------- CTA path
 
 #include "cta.cuh"
+#include "group.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
                  const CountOut& out, IntersectScratch& scr, cudaStream_t s) {
-  unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * 64u);
-  k_intersect_warp<TALLY, LIST, FILTER, WIDE, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
-      A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n);
+  // Apex groups pay off when oriented lists are short (they pack >= 2 apexes
+  // per 32 lanes: Watts-Strogatz, G(n,m), R-MAT's tail); PA-like lists
+  // (h ~ 20) rarely pair up, and the per-apex kernel is faster there.
+  const bool groups = g_warp_variant == 0 ? nu.avg_len <= 16.f : g_warp_variant == 2;
+  if (!groups) {  // one apex per warp iteration
+    unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * 64u);
+    k_intersect_warp<TALLY, LIST, FILTER, WIDE, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n);
+  } else {  // apex groups, contiguous item range per warp (resident grid)
+    const unsigned ggrid = grid_for(items, kGWarps * 32, 148u * 5u);
+    uint64_t chunk = items / ((uint64_t)ggrid * kGWarps * 8);  // >= 8 chunks per warp
+    chunk = chunk < 32 ? 32 : (chunk > 256 ? 256 : chunk);
+    k_intersect_group<TALLY, LIST, FILTER, WIDE, Apex><<<ggrid, kGWarps * 32, 0, s>>>(
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+        (uint32_t)chunk);
+  }
   TG_CHECK_LAUNCH();
   ++g_launches;
 }
@@ -372,8 +386,8 @@ void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
                  bool wide) {
   if (!items) return;
   scr.ensure(items, s);
-  // [0]: long-apex queue size, [1]: CTA work counter
-  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, 2 * sizeof(unsigned long long), s));
+  // [0]: long-apex queue size, [1]: CTA work counter, [2]: warp-path chunk counter
+  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, 3 * sizeof(unsigned long long), s));
   if (filter) {
     if (wide) launch_warp<TALLY, LIST, true, true>(A, items, nu, ulo, uhi, out, scr, s);
     else launch_warp<TALLY, LIST, true, false>(A, items, nu, ulo, uhi, out, scr, s);
@@ -417,10 +431,11 @@ __global__ void k_cc(const uint64_t* __restrict__ off, uint64_t n,
 }  // namespace
 
 uint32_t g_block_cap = 0;
+int g_warp_variant = 0;
 
 void IntersectScratch::ensure(uint64_t cap, cudaStream_t s) {
   if (big.n < cap) big.alloc(cap, s);
-  if (big_count.n < 2) big_count.alloc(2, s);
+  if (big_count.n < 3) big_count.alloc(3, s);
 }
 
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,

@@ -115,6 +115,7 @@ struct CsrView {
   const uint64_t* desc;
   const uint32_t* data;
   uint32_t base;
+  float avg_len = 0.f;  // host-side hint: mean list length (kernel choice)
 };
 
 // ---- build / orient (build.cu, orient.cu) ----
@@ -184,6 +185,8 @@ extern unsigned long long g_launches;
 // CTA-path shared-memory capacity in entries (0 = default); tests lower it
 // to exercise the global-memory search path on small graphs.
 extern uint32_t g_block_cap;
+// warp-path kernel: 0 = automatic, 1 = one apex per warp iteration, 2 = groups
+extern int g_warp_variant;
 
 inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 64u) {
   uint64_t g = (work + block - 1) / block;

@@ -145,7 +145,7 @@ def test_criterion9_clustering(small_golden):
             assert [float(x).hex() for x in cc.coefficient] == rec["cc"]
 
 
-def test_pa20000_all_engines(small_golden):
+def test_pa20000_all_engines(small_golden, warp_variant):
     rec = small_golden["pa20000"]
     g = T.build_graph(T.gen_pa(20000, 20, 3))
     off, adj = g.csr()
@@ -189,8 +189,15 @@ def test_generators_match_reference_streams(small_golden):
 # ------------------------------------------------ fresh cases vs the oracle
 
 
+@pytest.fixture(params=[1, 2], ids=["per-apex", "groups"])
+def warp_variant(request):
+    lib().tg_debug_set_warp_variant(request.param)
+    yield request.param
+    lib().tg_debug_set_warp_variant(0)
+
+
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_random_graphs_all_engines_costs(seed):
+def test_random_graphs_all_engines_costs(seed, warp_variant):
     rng = np.random.default_rng(seed)
     for _ in range(4):
         n = int(rng.integers(20, 120))
@@ -241,7 +248,7 @@ def test_edge_cases():
     assert rep.total == 1
 
 
-def test_long_lists_block_and_global_paths():
+def test_long_lists_block_and_global_paths(warp_variant):
     """Apex lists longer than the warp path (64) go to the CTA path; lists
     longer than the CTA's shared-memory capacity are searched in global
     memory.  Lower the capacity to exercise the global path on a small graph."""

@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--engines", action="store_true")
     a = ap.parse_args()
     L = lib()
+    if os.environ.get("TG_WARP_VARIANT"):
+        L.tg_debug_set_warp_variant(int(os.environ["TG_WARP_VARIANT"]))
     for name in a.configs:
         kind, p = CONFIGS[name]
         p = dict(p)
