@@ -39,6 +39,17 @@ struct tg_graph {
   std::vector<uint32_t> part_b;
   tgb::DevEff part;
   tgb::SurrogatePack pack;
+
+  // every device buffer the handle owns (release before the stream dies;
+  // re-home stream-ordered frees when the caller switches streams)
+  template <class F>
+  void for_each_buf(F&& f) {
+    f(g.off); f(g.adj); f(g.deg); f(g.dcode);
+    f(eff.off); f(eff.data); f(eff.desc);
+    f(scr.big); f(scr.big_count);
+    f(part.off); f(part.data); f(part.desc);
+    f(pack.desc); f(pack.doff);
+  }
 };
 
 namespace {
@@ -402,15 +413,8 @@ tg_status tg_graph_free(tg_graph* g) {
     cudaSetDevice(g->device);
     cudaStreamSynchronize(g->own);
     if (g->stream != g->own) cudaStreamSynchronize(g->stream);
-    {
-      // release buffers on the library stream before destroying it
-      g->g.off.release(); g->g.adj.release(); g->g.deg.release();
-      g->eff.off.release(); g->eff.data.release(); g->eff.desc.release();
-      g->part.desc.release();
-      g->scr.big.release(); g->scr.big_count.release();
-      g->part.off.release(); g->part.data.release();
-      g->pack.desc.release(); g->pack.doff.release();
-    }
+    // release buffers on their streams before destroying the library's own
+    g->for_each_buf([](auto& b) { b.release(); });
     cudaStreamSynchronize(g->own);
     if (g->stream != g->own) cudaStreamSynchronize(g->stream);
     cudaEventDestroy(g->ev0);
@@ -446,12 +450,7 @@ tg_status tg_set_stream(tg_graph* g, void* stream) {
       g->stream = ns;
       // DBuf frees are stream-ordered on the stream they were allocated on;
       // re-home them so later frees order after work on the new stream.
-      auto rehome = [&](auto& buf) { buf.s = ns; };
-      rehome(g->g.off); rehome(g->g.adj); rehome(g->g.deg);
-      rehome(g->eff.off); rehome(g->eff.data); rehome(g->eff.desc); rehome(g->part.desc);
-      rehome(g->scr.big); rehome(g->scr.big_count);
-      rehome(g->part.off); rehome(g->part.data);
-      rehome(g->pack.desc); rehome(g->pack.doff);
+      g->for_each_buf([&](auto& b) { b.s = ns; });
     }
   });
 }

@@ -12,9 +12,14 @@
 // 64-bit radix sort + unique of directed keys (u<<32|v) (CUB onesweep); the
 // degree order needs no sort at all on the hot path: "v precedes u" is the
 // comparison (deg v, v) < (deg u, u), evaluated against a 4 B/vertex degree
-// array that stays L2-resident (126 MB L2 holds 31M degrees).  Orientation is
-// count -> scan -> ballot-compacted fill, which keeps each N_v ID-sorted
-// (effective.hpp:13-16).
+// array that stays L2-resident (126 MB L2 holds 31M degrees); beyond ~32M
+// vertices the comparison reads a monotone 1-byte degree code instead (exact
+// degrees only on a bucket tie), which keeps the lookup table in L2.
+// Orientation of the whole graph is tile-per-warp (32 vertices, dynamically
+// claimed): COUNT writes a keep bitmask over the adjacency, a CUB scan gives
+// the compact offsets, FILL streams the mask and writes each N_v ID-sorted
+// (effective.hpp:13-16).  Vertices of degree > 256 go to a queue served by
+// a CTA-per-vertex kernel so hub lists do not stall a tile.
 #include <cub/cub.cuh>
 
 #include "tg_internal.cuh"
@@ -86,10 +91,36 @@ __global__ void k_offsets_from_keys(const uint64_t* __restrict__ keys, uint64_t 
   }
 }
 
-__global__ void k_degrees(const uint64_t* __restrict__ off, uint64_t n, uint32_t* __restrict__ deg) {
+__global__ void k_degrees(const uint64_t* __restrict__ off, uint64_t n, uint32_t* __restrict__ deg,
+                          uint8_t* __restrict__ dcode) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * blockDim.x)
-    deg[v] = (uint32_t)(off[v + 1] - off[v]);
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = (uint32_t)(off[v + 1] - off[v]);
+    deg[v] = d;
+    dcode[v] = degree_code(d);
+  }
+}
+
+// precedes(v, u) from the 1-byte codes, exact degrees only on a bucket tie
+__device__ __forceinline__ bool precedes_coded(uint8_t cv, uint32_t v, uint8_t cu, uint32_t u,
+                                               const uint32_t* __restrict__ deg) {
+  if (cv != cu) return cv < cu;
+  if (cv < 240) return v < u;  // equal exact degrees: tie broken by id
+  const uint32_t dv = deg[v], du = deg[u];
+  return dv < du || (dv == du && v < u);
+}
+
+// Order key of a vertex: its degree, or its 1-byte code when the degree array
+// would not stay L2-resident (n beyond ~32M vertices).
+template <bool CODED>
+__device__ __forceinline__ uint32_t okey(const uint32_t* __restrict__ deg,
+                                         const uint8_t* __restrict__ dcode, uint32_t v) {
+  return CODED ? (uint32_t)__ldg(dcode + v) : __ldg(deg + v);
+}
+template <bool CODED>
+__device__ __forceinline__ bool okey_precedes(uint32_t kv, uint32_t v, uint32_t ku, uint32_t u,
+                                              const uint32_t* __restrict__ deg) {
+  return CODED ? precedes_coded((uint8_t)kv, v, (uint8_t)ku, u, deg) : precedes(kv, v, ku, u);
 }
 
 // ---------------------------------------------------------------- orientation
@@ -196,13 +227,15 @@ constexpr uint32_t kOBig = 256;  // degree above which a vertex leaves its tile
 // tile's item space (so a hub cannot stall one warp), and they are handled by
 // k_orient_big (32 lanes per vertex) from a queue the COUNT pass fills.
 // Tiles are claimed dynamically (tile_ctr).
-template <bool FILL>
+template <bool FILL, bool CODED>
 __global__ void __launch_bounds__(kOWarps * 32, 5)
 k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-               const uint32_t* __restrict__ deg, uint64_t n, uint64_t* __restrict__ cnt_or_eoff,
+               const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode, uint64_t n,
+               uint64_t* __restrict__ cnt_or_eoff,
                uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff,
                unsigned long long* __restrict__ tile_ctr, uint32_t* __restrict__ bigq,
-               unsigned long long* __restrict__ bigq_n, uint32_t* __restrict__ kmask) {
+               unsigned long long* __restrict__ bigq_n, uint32_t* __restrict__ kmask,
+               const uint64_t* __restrict__ hcnt) {
   __shared__ uint32_t sTbl[kOWarps][kOTbl + kOUnroll];
   __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
   __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
@@ -220,7 +253,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     const uint64_t v = v0 + lane;
     const bool valid = v < n;
     const uint64_t my_b = valid ? off[v] : 0, my_e = valid ? off[v + 1] : 0;
-    const uint32_t my_dv = valid ? deg[v] : 0;
+    const uint32_t my_dv = valid ? okey<CODED>(deg, dcode, (uint32_t)v) : 0;  // order key
     const uint64_t tile_b = __shfl_sync(FULL, my_b, 0);
     const uint32_t len = (uint32_t)(my_e - my_b);
     const bool big = len > kOBig;
@@ -247,8 +280,8 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     if (FILL) {
       uint64_t my_o = valid ? cnt_or_eoff[v] : 0;
       out_b = __shfl_sync(FULL, my_o, 0);
-      uint32_t hk = 0;  // kept entries of this (non-big) vertex
-      if (valid && !big) hk = (uint32_t)(cnt_or_eoff[v + 1] - my_o);
+      uint32_t hk = 0;  // kept entries of this (non-big) vertex (lists are padded)
+      if (valid && !big) hk = (uint32_t)hcnt[v];
       uint32_t kst = hk;  // exclusive prefix of non-big kept counts
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -306,9 +339,9 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
             const uint32_t vm = base >= wend ? 0u
                                 : (wend - base >= 32 ? FULL : ((1u << (wend - base)) - 1u));
             kms[q] = (sh ? ((lo >> sh) | (hi << (32 - sh))) : lo) & vm;
-            us[q] = ((kms[q] >> lane) & 1u) ? adj[tile_b + ash + idx] : 0u;
+            us[q] = ((kms[q] >> lane) & 1u) ? __ldcs(adj + tile_b + ash + idx) : 0u;
           } else {
-            us[q] = idx < wend ? adj[tile_b + ash + idx] : 0u;
+            us[q] = idx < wend ? __ldcs(adj + tile_b + ash + idx) : 0u;
           }
         }
         if (FILL) {
@@ -323,7 +356,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
           uint32_t dus[kOUnroll];
 #pragma unroll
           for (int q = 0; q < kOUnroll; ++q)
-            dus[q] = (base0 + 32 * q + lane < wend) ? deg[us[q]] : 0u;
+            dus[q] = (base0 + 32 * q + lane < wend) ? okey<CODED>(deg, dcode, us[q]) : 0u;
 #pragma unroll
           for (int q = 0; q < kOUnroll; ++q) {
             const uint32_t base = base0 + 32 * q;
@@ -331,7 +364,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
             const uint32_t jj = jjs[q];
             const uint32_t sv = __shfl_sync(FULL, c_v, jj);
             const uint32_t sdv = __shfl_sync(FULL, c_dv, jj);
-            const bool keep = idx < wend && precedes(sdv, sv, dus[q], us[q]);
+            const bool keep = idx < wend && okey_precedes<CODED>(sdv, sv, dus[q], us[q], deg);
             const unsigned km = __ballot_sync(FULL, keep);
             const uint32_t send = __shfl_sync(FULL, c_end, jj);
             if (idx < wend && idx + 1 == send) sCum[w][jj] = kept + __popc(km & le_mask);
@@ -362,10 +395,11 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
 
 // Big vertices: 32 lanes per vertex over a device-side queue.  COUNT writes
 // h_v; FILL writes N_v at eoff[v] in adjacency order (ballot prefix).
-template <bool FILL>
+template <bool FILL, bool CODED>
 __global__ void __launch_bounds__(256)
 k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-             const uint32_t* __restrict__ deg, const uint32_t* __restrict__ bigq,
+             const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode,
+             const uint32_t* __restrict__ bigq,
              const unsigned long long* __restrict__ bigq_n, uint64_t* __restrict__ cnt_or_eoff,
              uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff,
              uint32_t* __restrict__ kmask) {
@@ -383,7 +417,7 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nq; i += warps) {
     const uint32_t v = bigq[i];
     const uint64_t b = off[v], e = off[v + 1];
-    const uint32_t dv = deg[v];
+    const uint32_t cv = okey<CODED>(deg, dcode, v);
     const uint64_t ob = FILL ? cnt_or_eoff[v] : 0;
     uint64_t c = 0;
     for (uint64_t k0 = b; k0 < e; k0 += 64) {
@@ -393,16 +427,16 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
       if (FILL) {
         m1 = mask_at(k0, e);
         m2 = k0 + 32 < e ? mask_at(k0 + 32, e) : 0u;
-        u1 = ((m1 >> lane) & 1u) ? adj[k1] : 0u;
-        u2 = ((m2 >> lane) & 1u) ? adj[k2] : 0u;
+        u1 = ((m1 >> lane) & 1u) ? __ldcs(adj + k1) : 0u;
+        u2 = ((m2 >> lane) & 1u) ? __ldcs(adj + k2) : 0u;
         if ((m1 >> lane) & 1u) eff[ob + c + __popc(m1 & lt_mask)] = u1;
         if ((m2 >> lane) & 1u) eff[ob + c + __popc(m1) + __popc(m2 & lt_mask)] = u2;
       } else {
-        u1 = k1 < e ? adj[k1] : 0u;
-        u2 = k2 < e ? adj[k2] : 0u;
-        const uint32_t d1 = k1 < e ? deg[u1] : 0u, d2 = k2 < e ? deg[u2] : 0u;
-        const bool p1 = k1 < e && precedes(dv, v, d1, u1);
-        const bool p2 = k2 < e && precedes(dv, v, d2, u2);
+        u1 = k1 < e ? __ldcs(adj + k1) : 0u;
+        u2 = k2 < e ? __ldcs(adj + k2) : 0u;
+        const uint32_t c1 = k1 < e ? okey<CODED>(deg, dcode, u1) : 0, c2 = k2 < e ? okey<CODED>(deg, dcode, u2) : 0;
+        const bool p1 = k1 < e && okey_precedes<CODED>(cv, v, c1, u1, deg);
+        const bool p2 = k2 < e && okey_precedes<CODED>(cv, v, c2, u2, deg);
         m1 = __ballot_sync(0xffffffffu, p1);
         m2 = __ballot_sync(0xffffffffu, p2);
         if (lane < 2) {
@@ -610,8 +644,9 @@ void build_graph_device(const uint32_t* d_pairs, uint64_t E, uint64_t n_override
 
 void compute_degrees(DevGraph& g, cudaStream_t s) {
   g.deg.alloc(g.n ? g.n : 1, s);
+  g.dcode.alloc(g.n ? g.n : 1, s);
   if (g.n) {
-    k_degrees<<<grid_for(g.n, 256), 256, 0, s>>>(g.off.p, g.n, g.deg.p);
+    k_degrees<<<grid_for(g.n, 256), 256, 0, s>>>(g.off.p, g.n, g.deg.p, g.dcode.p);
     TG_CHECK_LAUNCH();
     ++g_launches;
   }
@@ -648,6 +683,39 @@ void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cud
   out.entries = entries;
 }
 
+template <bool CODED>
+static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
+  const uint64_t ntiles = (g.n + 31) / 32;
+  const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
+  DBuf<uint64_t> cnt(g.n, s);
+  DBuf<uint32_t> bigq(g.n, s);
+  DBuf<unsigned long long> ctr(3, s);  // tile counters (count, fill), big-queue size
+  ctr.zero();
+  // keep-decision bitmasks (tiles: compressed item space; big: real positions)
+  const uint64_t mwords = g.m2 / 32 + 8;
+  DBuf<uint32_t> kmask(2 * mwords, s);
+  kmask.zero();
+  k_orient_tiles<false, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, cnt.p,
+                                                      nullptr, nullptr, ctr.p, bigq.p, ctr.p + 2,
+                                                      kmask.p, nullptr);
+  TG_CHECK_LAUNCH();
+  k_orient_big<false, CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p, ctr.p + 2, cnt.p,
+                                              nullptr, nullptr, kmask.p + mwords);
+  TG_CHECK_LAUNCH();
+  TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::InclusiveSum(t, b, cnt.p, out.off.p + 1, (int64_t)g.n, s);
+  });
+  k_orient_tiles<true, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, out.off.p,
+                                                     out.desc.p, out.data.p, ctr.p + 1, nullptr,
+                                                     nullptr, kmask.p, cnt.p);
+  TG_CHECK_LAUNCH();
+  k_orient_big<true, CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p, ctr.p + 2,
+                                             out.off.p, out.desc.p, out.data.p, kmask.p + mwords);
+  TG_CHECK_LAUNCH();
+  g_launches += 6;  // count, big count, scan (init + sweep), fill, big fill
+}
+
 // effective.hpp:37-52 for the whole graph (the hot path): tile-streamed
 // count -> CUB scan -> tile-streamed fill, compact layout, no host sync
 // (sum h_v = m is known).
@@ -660,40 +728,16 @@ void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t m = g.m2 / 2;
   if (out.desc.n < (g.n ? g.n : 1)) out.desc.alloc(g.n ? g.n : 1, s);
   if (out.off.n < g.n + 1) out.off.alloc(g.n + 1, s);
+  // (padding list starts to 32 B was measured: no gain on C2, so lists are
+  // packed back to back)
   if (out.data.n < (m ? m : 1)) out.data.alloc(m ? m : 1, s);
   if (!g.n) {
     TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
     return;
   }
-  const uint64_t ntiles = (g.n + 31) / 32;
-  const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
-  DBuf<uint64_t> cnt(g.n, s);
-  DBuf<uint32_t> bigq(g.n, s);
-  DBuf<unsigned long long> ctr(3, s);  // tile counters (count, fill), big-queue size
-  ctr.zero();
-  // keep-decision bitmasks (tiles: compressed item space; big: real positions)
-  const uint64_t mwords = g.m2 / 32 + 8;
-  DBuf<uint32_t> kmask(2 * mwords, s);
-  kmask.zero();
-  k_orient_tiles<false><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.n, cnt.p,
-                                                      nullptr, nullptr, ctr.p, bigq.p, ctr.p + 2,
-                                                      kmask.p);
-  TG_CHECK_LAUNCH();
-  k_orient_big<false><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, bigq.p, ctr.p + 2, cnt.p,
-                                              nullptr, nullptr, kmask.p + mwords);
-  TG_CHECK_LAUNCH();
-  TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
-  cub_run(s, [&](void* t, size_t& b) {
-    return cub::DeviceScan::InclusiveSum(t, b, cnt.p, out.off.p + 1, (int64_t)g.n, s);
-  });
-  k_orient_tiles<true><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.n, out.off.p,
-                                                     out.desc.p, out.data.p, ctr.p + 1, nullptr,
-                                                     nullptr, kmask.p);
-  TG_CHECK_LAUNCH();
-  k_orient_big<true><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, bigq.p, ctr.p + 2,
-                                             out.off.p, out.desc.p, out.data.p, kmask.p + mwords);
-  TG_CHECK_LAUNCH();
-  g_launches += 6;  // count, big count, scan (init + sweep), fill, big fill
+  // 1-byte degree codes once the 4-byte degrees would not stay in L2
+  if (g.n > (32ull << 20)) orient_tiles<true>(g, out, s);
+  else orient_tiles<false>(g, out, s);
 }
 
 // Gappy single-pass orientation (N_v in the first h_v slots of v's symmetric

@@ -84,7 +84,22 @@ struct DevGraph {
   DBuf<uint64_t> off;      // n+1
   DBuf<uint32_t> adj;      // m2
   DBuf<uint32_t> deg;      // n
+  DBuf<uint8_t> dcode;     // n: monotone 1-byte degree code (orientation)
 };
+
+// Monotone 1-byte code of a degree: exact below 240, then one bucket per
+// doubling.  code(a) < code(b) implies a < b; equal codes below 240 imply
+// equal degrees; equal codes >= 240 need the exact degrees.  A 1-byte
+// lookup table of n vertices stays L2-resident 4x longer than the degrees.
+__host__ __device__ __forceinline__ uint8_t degree_code(uint32_t d) {
+  if (d < 240) return (uint8_t)d;
+  uint32_t c = 240, x = d / 240;  // x >= 1
+  while (x > 1 && c < 255) {
+    x >>= 1;
+    c += 4;
+  }
+  return (uint8_t)(c > 255 ? 255 : c);
+}
 
 // Packed list descriptor: (start << 24) | len.  One 8-byte load gives a
 // list's position and length (len < 2^24, start < 2^40).

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--parts", type=int, default=4096)
     ap.add_argument("--spot", type=int, default=6)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--quick", action="store_true", help="timing only (no engines / oracle)")
     a = ap.parse_args()
     rec = {"config": f"gen_pa({a.n},{a.d},{a.seed})"}
     t0 = time.time()
@@ -68,6 +69,9 @@ def main():
     T_ = int(d.item())
     rec["triangles"] = T_
     torch.cuda.set_stream(torch.cuda.default_stream())
+    if a.quick:
+        print(json.dumps(rec), flush=True)
+        return
     for eng in (T.EngineKind.Aop, T.EngineKind.AnopSurrogate):
         rep = T.run_engine(g, T.EngineConfig(engine=eng, ranks=8))
         rec[f"{T.to_string(eng)}8_total"] = rep.total
