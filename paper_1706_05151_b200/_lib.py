@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrigraph_b200.so")
+# TG_LIB_PATH: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("TG_LIB_PATH") or os.path.join(HERE, "libtrigraph_b200.so")
 
 TG_OK = 0
 TG_ERR_INVALID_ARGUMENT = 1

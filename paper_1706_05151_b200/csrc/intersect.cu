@@ -107,7 +107,15 @@ __device__ __forceinline__ bool contains_small(const uint32_t* a, uint32_t n, ui
   return pos < n && a[pos] == x;
 }
 constexpr int kTblWords = 32;   // segment-start table window: 1024 items
-constexpr int kUnroll = 4;      // chunks (of 32 items) in flight per warp
+#ifndef TG_UNROLL
+#define TG_UNROLL 4
+#endif
+#ifndef TG_WBLOCKS
+#define TG_WBLOCKS 6
+#endif
+constexpr int kUnroll = 4;      // chunks (of 32 items) in flight per warp (group kernel)
+constexpr int kWUnroll = TG_UNROLL;  // ... in the per-apex warp kernel
+constexpr int kWBlocks = TG_WBLOCKS; // resident blocks per SM of the per-apex warp kernel
 constexpr uint32_t kWarpWork = 4096;  // items of the first u-batch above which
                                       // an apex moves to the CTA path
 // Sentinel for "no item" / "empty slot": 0xffffffff is never a NodeId of an
@@ -169,14 +177,14 @@ struct Ht4 {
 // FILTER restricts the middle vertex to [ulo, uhi) (SurrogateCount's core
 // range); WIDE selects 64-bit element indexing (> 2^32 list entries).
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 6)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kWBlocks)
 k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                  uint32_t* __restrict__ big, unsigned long long* __restrict__ big_count,
-                 uint64_t big_cap) {
+                 uint64_t big_cap, unsigned long long* __restrict__ chunk_ctr, uint32_t chunk) {
   using Adj = typename std::conditional<WIDE, long long, uint32_t>::type;
   __shared__ uint32_t sNv[kWarpsPerBlock][kWCap];
   __shared__ uint32_t sBm[kWarpsPerBlock][kBmWords];
-  __shared__ uint32_t sTbl[kWarpsPerBlock][kTblWords + kUnroll];
+  __shared__ uint32_t sTbl[kWarpsPerBlock][kTblWords + kWUnroll];
   __shared__ Adj sAdj[kWarpsPerBlock][32];
   __shared__ uint32_t sSt[kWarpsPerBlock][32];
   __shared__ uint32_t sU[kWarpsPerBlock][32];
@@ -194,16 +202,25 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   unsigned long long acc = 0;
   __syncwarp();
 
-  for (uint64_t k = (uint64_t)blockIdx.x * kWarpsPerBlock + w; k < nitems;
-       k += (uint64_t)gridDim.x * kWarpsPerBlock) {
+  // resident grid; warps claim runs of `chunk` consecutive apexes
+  uint64_t k = 0, kend = 0;
+  for (;;) {
+    if (k == kend) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(chunk_ctr, (unsigned long long)chunk);
+      k = __shfl_sync(FULL, c, 0);
+      if (k >= nitems) break;
+      kend = min(nitems, k + chunk);
+    }
+    const uint64_t kc = k++;
     uint32_t v, hv;
     const uint32_t* L;
-    A.get(k, v, L, hv);
+    A.get(kc, v, L, hv);
     if (hv < 2) continue;  // a triangle needs u, w ∈ N_v
     if (hv > kWCap) {
       if (lane == 0) {
         unsigned long long pos = atomicAdd(big_count, 1ull);
-        if (pos < big_cap) big[pos] = (uint32_t)k;
+        if (pos < big_cap) big[pos] = (uint32_t)kc;
       }
       continue;
     }
@@ -248,7 +265,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         // whole apex to the CTA path so one warp cannot become a straggler
         if (lane == 0) {
           unsigned long long pos = atomicAdd(big_count, 1ull);
-          if (pos < big_cap) big[pos] = (uint32_t)k;
+          if (pos < big_cap) big[pos] = (uint32_t)kc;
         }
         break;
       }
@@ -270,16 +287,16 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       uint32_t cnt = 0;  // segment starts before the current chunk
       for (uint32_t w0 = 0; w0 < S; w0 += 32 * kTblWords) {
         Tbl[lane] = 0;
-        if (lane < kUnroll) Tbl[kTblWords + lane] = 0;
+        if (lane < kWUnroll) Tbl[kTblWords + lane] = 0;
         __syncwarp();
         if (has && my_st >= w0 && my_st < w0 + 32 * kTblWords)
           atomicOr(&Tbl[(my_st - w0) >> 5], 1u << (my_st & 31));
         __syncwarp();
         const uint32_t wend = min(S, w0 + 32 * kTblWords);
-        for (uint32_t base0 = w0; base0 < wend; base0 += 32 * kUnroll) {
-          uint32_t xs[kUnroll], jjs[kUnroll];
+        for (uint32_t base0 = w0; base0 < wend; base0 += 32 * kWUnroll) {
+          uint32_t xs[kWUnroll], jjs[kWUnroll];
 #pragma unroll
-          for (int q = 0; q < kUnroll; ++q) {
+          for (int q = 0; q < kWUnroll; ++q) {
             const uint32_t base = base0 + 32 * q;
             const uint32_t word = Tbl[(base - w0) >> 5];  // padded: 0 past the window
             const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
@@ -293,7 +310,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
           // filter: one conflict-light LDS.32 per item
           unsigned hits = 0;
 #pragma unroll
-          for (int q = 0; q < kUnroll; ++q) {
+          for (int q = 0; q < kWUnroll; ++q) {
             const uint32_t h = bm_hash(xs[q]), bm = bm_mask(h);
             hits |= (unsigned)(((Bm[bm_word(h)] & bm) == bm) & (xs[q] != kNoItem)) << q;
           }
@@ -302,11 +319,11 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
           // sorted N_v (cheaper than a bucket probe at PA/WS list lengths)
           unsigned fnd = 0;
 #pragma unroll
-          for (int q = 0; q < kUnroll; ++q)
+          for (int q = 0; q < kWUnroll; ++q)
             if ((hits >> q) & 1u) fnd |= (unsigned)contains_small(Nv, hv, xs[q]) << q;
           if (!__any_sync(FULL, fnd != 0)) continue;
 #pragma unroll
-          for (int q = 0; q < kUnroll; ++q) {
+          for (int q = 0; q < kWUnroll; ++q) {
             const uint32_t x = xs[q];
             const bool found = (fnd >> q) & 1u;
             {
@@ -354,9 +371,12 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // (h ~ 20) rarely pair up, and the per-apex kernel is faster there.
   const bool groups = g_warp_variant == 0 ? nu.avg_len <= 16.f : g_warp_variant == 2;
   if (!groups) {  // one apex per warp iteration
-    unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * 64u);
+    const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kWBlocks);  // resident
+    uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);   // >= 16 runs per warp
+    chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
     k_intersect_warp<TALLY, LIST, FILTER, WIDE, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
-        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n);
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+        (uint32_t)chunk);
   } else {  // apex groups, contiguous item range per warp (resident grid)
     const unsigned ggrid = grid_for(items, kGWarps * 32, 148u * 5u);
     uint64_t chunk = items / ((uint64_t)ggrid * kGWarps * 8);  // >= 8 chunks per warp

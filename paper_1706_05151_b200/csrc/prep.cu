@@ -91,14 +91,21 @@ __global__ void k_offsets_from_keys(const uint64_t* __restrict__ keys, uint64_t 
   }
 }
 
+// degrees, their 1-byte codes, and the sum of degrees above `big` (the
+// orientation's hub threshold: size of its separate hub-list region)
 __global__ void k_degrees(const uint64_t* __restrict__ off, uint64_t n, uint32_t* __restrict__ deg,
-                          uint8_t* __restrict__ dcode) {
+                          uint8_t* __restrict__ dcode, uint32_t big,
+                          unsigned long long* __restrict__ big_sum) {
+  unsigned long long bs = 0;
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t d = (uint32_t)(off[v + 1] - off[v]);
     deg[v] = d;
     dcode[v] = degree_code(d);
+    if (d > big) bs += d;
   }
+  for (int o = 16; o > 0; o >>= 1) bs += __shfl_xor_sync(0xffffffffu, bs, o);
+  if ((threadIdx.x & 31) == 0 && bs) atomicAdd(big_sum, bs);
 }
 
 // precedes(v, u) from the 1-byte codes, exact degrees only on a bucket tie
@@ -227,7 +234,11 @@ constexpr uint32_t kOBig = 256;  // degree above which a vertex leaves its tile
 // tile's item space (so a hub cannot stall one warp), and they are handled by
 // k_orient_big (32 lanes per vertex) from a queue the COUNT pass fills.
 // Tiles are claimed dynamically (tile_ctr).
-template <bool FILL, bool CODED>
+//   ONE  : single pass (the hot path): kept item k of the tile goes to
+//          eff[tile_b + k] -- each tile's lists back to back at the start of
+//          the tile's own adjacency range (ID-sorted, vertex order), no mask,
+//          no scan; big vertices write above m2 (k_orient_big1).
+template <int MODE, bool CODED>
 __global__ void __launch_bounds__(kOWarps * 32, 5)
 k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode, uint64_t n,
@@ -239,6 +250,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
   __shared__ uint32_t sTbl[kOWarps][kOTbl + kOUnroll];
   __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
   __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
+  constexpr bool FILL = MODE == 1, ONE = MODE == 2;
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
@@ -269,7 +281,8 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     est -= elen;
     if (S == 0) {
       if (valid && !big) {
-        if (!FILL) cnt_or_eoff[v] = 0;
+        if (ONE) edesc[v] = make_desc(0, 0);
+        else if (!FILL) cnt_or_eoff[v] = 0;
         else edesc[v] = make_desc(cnt_or_eoff[v], 0);
       }
       continue;
@@ -368,7 +381,8 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
             const unsigned km = __ballot_sync(FULL, keep);
             const uint32_t send = __shfl_sync(FULL, c_end, jj);
             if (idx < wend && idx + 1 == send) sCum[w][jj] = kept + __popc(km & le_mask);
-            if (lane == 0 && km) {  // record the decisions for the FILL pass
+            if (ONE && keep) eff[tile_b + kept + __popc(km & lt_mask)] = us[q];
+            if (!ONE && lane == 0 && km) {  // record the decisions for the FILL pass
               const uint64_t pos = tile_b + base;
               const uint32_t sh = (uint32_t)(pos & 31);
               atomicOr(&kmask[pos >> 5], km << sh);
@@ -382,12 +396,14 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     }
     __syncwarp();
     if (!FILL && valid && !big) {
-      uint32_t h = 0;
+      uint32_t h = 0, hb = 0;
       if (elen > 0) {
         const uint32_t c = __popc(ne & lt_mask);
-        h = sCum[w][c] - (c ? sCum[w][c - 1] : 0u);
+        hb = c ? sCum[w][c - 1] : 0u;
+        h = sCum[w][c] - hb;
       }
-      cnt_or_eoff[v] = h;
+      if (ONE) edesc[v] = make_desc(tile_b + hb, h);
+      else cnt_or_eoff[v] = h;
     }
     __syncwarp();
   }
@@ -455,6 +471,52 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
       if (FILL) edesc[v] = make_desc(ob, c);
       else cnt_or_eoff[v] = c;
     }
+  }
+}
+
+// Big vertices, single pass: v's list goes to a region above m2 reserved
+// with one atomic per vertex (d_v slots, h_v used); 32 lanes x kBigU entries
+// per iteration keep several adjacency loads and degree lookups in flight.
+constexpr int kBigU = 4;
+template <bool CODED>
+__global__ void __launch_bounds__(256)
+k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+              const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode,
+              const uint32_t* __restrict__ bigq, const unsigned long long* __restrict__ bigq_n,
+              uint64_t m2, unsigned long long* __restrict__ cursor, uint64_t* __restrict__ edesc,
+              uint32_t* __restrict__ eff) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint64_t nq = *bigq_n;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nq; i += warps) {
+    const uint32_t v = bigq[i];
+    const uint64_t b = off[v], e = off[v + 1];
+    const uint32_t cv = okey<CODED>(deg, dcode, v);
+    unsigned long long ob = 0;
+    if (lane == 0) ob = atomicAdd(cursor, (unsigned long long)(e - b));
+    ob = m2 + __shfl_sync(0xffffffffu, ob, 0);
+    uint64_t c = 0;
+    for (uint64_t k0 = b; k0 < e; k0 += 32 * kBigU) {
+      uint32_t us[kBigU], ks[kBigU];
+#pragma unroll
+      for (int q = 0; q < kBigU; ++q) {
+        const uint64_t k = k0 + 32 * q + lane;
+        us[q] = k < e ? __ldcs(adj + k) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < kBigU; ++q)
+        ks[q] = (k0 + 32 * q + lane < e) ? okey<CODED>(deg, dcode, us[q]) : 0u;
+#pragma unroll
+      for (int q = 0; q < kBigU; ++q) {
+        const bool keep =
+            k0 + 32 * q + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg);
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (keep) eff[ob + c + __popc(km & lt_mask)] = us[q];
+        c += __popc(km);
+      }
+    }
+    if (lane == 0) edesc[v] = make_desc(ob, c);
   }
 }
 
@@ -645,10 +707,17 @@ void build_graph_device(const uint32_t* d_pairs, uint64_t E, uint64_t n_override
 void compute_degrees(DevGraph& g, cudaStream_t s) {
   g.deg.alloc(g.n ? g.n : 1, s);
   g.dcode.alloc(g.n ? g.n : 1, s);
+  g.big_entries = 0;
   if (g.n) {
-    k_degrees<<<grid_for(g.n, 256), 256, 0, s>>>(g.off.p, g.n, g.deg.p, g.dcode.p);
+    DBuf<unsigned long long> bs(1, s);
+    bs.zero();
+    k_degrees<<<grid_for(g.n, 256), 256, 0, s>>>(g.off.p, g.n, g.deg.p, g.dcode.p, kOBig, bs.p);
     TG_CHECK_LAUNCH();
     ++g_launches;
+    unsigned long long h = 0;
+    TG_CUDA(cudaMemcpyAsync(&h, bs.p, 8, cudaMemcpyDeviceToHost, s));
+    TG_CUDA(cudaStreamSynchronize(s));
+    g.big_entries = h;
   }
 }
 
@@ -695,7 +764,7 @@ static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t mwords = g.m2 / 32 + 8;
   DBuf<uint32_t> kmask(2 * mwords, s);
   kmask.zero();
-  k_orient_tiles<false, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, cnt.p,
+  k_orient_tiles<0, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, cnt.p,
                                                       nullptr, nullptr, ctr.p, bigq.p, ctr.p + 2,
                                                       kmask.p, nullptr);
   TG_CHECK_LAUNCH();
@@ -706,7 +775,7 @@ static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   cub_run(s, [&](void* t, size_t& b) {
     return cub::DeviceScan::InclusiveSum(t, b, cnt.p, out.off.p + 1, (int64_t)g.n, s);
   });
-  k_orient_tiles<true, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, out.off.p,
+  k_orient_tiles<1, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, out.off.p,
                                                      out.desc.p, out.data.p, ctr.p + 1, nullptr,
                                                      nullptr, kmask.p, cnt.p);
   TG_CHECK_LAUNCH();
@@ -716,10 +785,46 @@ static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   g_launches += 6;  // count, big count, scan (init + sweep), fill, big fill
 }
 
-// effective.hpp:37-52 for the whole graph (the hot path): tile-streamed
-// count -> CUB scan -> tile-streamed fill, compact layout, no host sync
-// (sum h_v = m is known).
+template <bool CODED>
+static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
+  const uint64_t ntiles = (g.n + 31) / 32;
+  const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
+  DBuf<uint32_t> bigq(g.n, s);
+  DBuf<unsigned long long> ctr(3, s);  // tile counter, big-queue size, big-region cursor
+  ctr.zero();
+  k_orient_tiles<2, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n,
+                                                         nullptr, out.desc.p, out.data.p, ctr.p,
+                                                         bigq.p, ctr.p + 1, nullptr, nullptr);
+  TG_CHECK_LAUNCH();
+  k_orient_big1<CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p,
+                                               ctr.p + 1, g.m2, ctr.p + 2, out.desc.p, out.data.p);
+  TG_CHECK_LAUNCH();
+  g_launches += 2;
+}
+
+// effective.hpp:37-52 for the whole graph (the hot path), no host sync.
+//  * tile layout (default): ONE streaming pass; each tile's lists sit back
+//    to back at the start of the tile's adjacency range, big vertices above
+//    m2 -- list descriptors carry the positions;
+//  * compact layout (when the tile layout would need 64-bit element indices,
+//    > 2^32 slots): count -> CUB scan -> fill, lists back to back.
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
+  TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
+  const uint64_t slots = g.m2 + g.big_entries;
+  if (!g.n || slots >= (1ull << 32)) return orient_full_compact(g, out, s);
+  out.rows = g.n;
+  out.base = 0;
+  out.compact = false;
+  out.entries = g.m2 / 2;
+  if (out.desc.n < g.n) out.desc.alloc(g.n, s);
+  if (out.data.n < (slots ? slots : 1)) out.data.alloc(slots ? slots : 1, s);
+  out.off.release();
+  if (g.n > (32ull << 20)) orient_onepass<true>(g, out, s);
+  else orient_onepass<false>(g, out, s);
+}
+
+// count -> CUB scan -> fill, compact layout (sum h_v = m is known).
+void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s) {
   TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
   out.rows = g.n;
   out.base = 0;

@@ -85,6 +85,7 @@ struct DevGraph {
   DBuf<uint32_t> adj;      // m2
   DBuf<uint32_t> deg;      // n
   DBuf<uint8_t> dcode;     // n: monotone 1-byte degree code (orientation)
+  uint64_t big_entries = 0;  // sum of degrees of the orientation's hub vertices
 };
 
 // Monotone 1-byte code of a degree: exact below 240, then one bucket per
@@ -140,8 +141,9 @@ void compute_degrees(DevGraph& g, cudaStream_t s);
 // Orient rows [vlo, vhi) of g into `out` (out.base = vlo), compact layout;
 // lists ID-sorted.
 void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s);
-// Orient the whole graph in one pass, gappy layout (no host sync).
+// Orient the whole graph (no host sync): one-pass tile layout, or compact.
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s);
+void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
 // sum of list lengths over rows [lo, hi) (host result).
