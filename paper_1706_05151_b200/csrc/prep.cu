@@ -229,6 +229,7 @@ constexpr int kOTbl = 32;       // table window: 1024 items
 constexpr int kOUnroll = 4;
 
 constexpr uint32_t kOBig = 256;  // degree above which a vertex leaves its tile
+constexpr uint32_t kOHub = 4096;  // ... and above which a whole CTA orients it (ONE mode)
 
 // Tiles skip "big" vertices (degree > kOBig): their items are removed from the
 // tile's item space (so a hub cannot stall one warp), and they are handled by
@@ -269,7 +270,11 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     const uint64_t tile_b = __shfl_sync(FULL, my_b, 0);
     const uint32_t len = (uint32_t)(my_e - my_b);
     const bool big = len > kOBig;
-    if (!FILL && big) bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
+    if (!FILL && !ONE && big) bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
+    if (ONE && big) {  // hubs (> kOHub) from the back of the queue, one CTA each
+      if (len > kOHub) bigq[n - 1 - atomicAdd(bigq_n + 2, 1ull)] = (uint32_t)v;
+      else bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
+    }
     const uint32_t elen = big ? 0u : len;  // length in the tile's item space
     uint32_t est = elen;                   // -> exclusive prefix of elen
 #pragma unroll
@@ -475,28 +480,104 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
 }
 
 // Big vertices, single pass: v's list goes to a region above m2 reserved
-// with one atomic per vertex (d_v slots, h_v used); 32 lanes x kBigU entries
-// per iteration keep several adjacency loads and degree lookups in flight.
+// with one atomic per vertex (d_v slots, h_v used).
+//  * hubs (d > kOHub, back of the queue): one 256-thread CTA per hub, in
+//    8192-entry segments -- keep masks of the 256 32-entry chunks in shared
+//    memory, a block scan of their popcounts, then the kept entries are
+//    written (re-read from L1/L2) in adjacency order;
+//  * the rest (kOBig < d <= kOHub): one warp per vertex, 32 x kBigU entries
+//    per iteration so several loads and lookups are in flight.
+// Counters: c[1] medium queue size, c[2] region cursor, c[3] hub queue size,
+// c[4] hub claims, c[5] medium claims.
 constexpr int kBigU = 4;
 template <bool CODED>
 __global__ void __launch_bounds__(256)
 k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
               const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode,
-              const uint32_t* __restrict__ bigq, const unsigned long long* __restrict__ bigq_n,
-              uint64_t m2, unsigned long long* __restrict__ cursor, uint64_t* __restrict__ edesc,
-              uint32_t* __restrict__ eff) {
-  const unsigned lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const uint64_t nq = *bigq_n;
-  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nq; i += warps) {
+              const uint32_t* __restrict__ bigq, uint64_t n, unsigned long long* __restrict__ c,
+              uint64_t m2, uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff) {
+  __shared__ uint32_t sM[256], sO[256], sW[8];
+  __shared__ unsigned long long sI, sBase;
+  const unsigned t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const unsigned FULL = 0xffffffffu, lt_mask = (1u << lane) - 1u;
+  const uint64_t nh = c[3];
+  for (;;) {  // hubs: one CTA each
+    if (t == 0) sI = atomicAdd(c + 4, 1ull);
+    __syncthreads();
+    const uint64_t i = sI;
+    if (i >= nh) break;
+    const uint32_t v = bigq[n - 1 - i];
+    const uint64_t b = off[v], e = off[v + 1];
+    const uint32_t cv = okey<CODED>(deg, dcode, v);
+    if (t == 0) sBase = m2 + atomicAdd(c + 2, (unsigned long long)(e - b));
+    __syncthreads();
+    const uint64_t ob = sBase;
+    uint64_t kept = 0;
+    for (uint64_t s0 = b; s0 < e; s0 += 8192) {
+      const uint64_t wb = s0 + 1024 * w;  // this warp's 32 chunks
+      for (int ch0 = 0; ch0 < 32; ch0 += kBigU) {
+        uint32_t us[kBigU], ks[kBigU];
+#pragma unroll
+        for (int q = 0; q < kBigU; ++q) {
+          const uint64_t k = wb + 32 * (ch0 + q) + lane;
+          us[q] = k < e ? __ldg(adj + k) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kBigU; ++q)
+          ks[q] = (wb + 32 * (ch0 + q) + lane < e) ? okey<CODED>(deg, dcode, us[q]) : 0u;
+#pragma unroll
+        for (int q = 0; q < kBigU; ++q) {
+          const bool keep =
+              wb + 32 * (ch0 + q) + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg);
+          const unsigned km = __ballot_sync(FULL, keep);
+          if (lane == 0) sM[32 * w + ch0 + q] = km;
+        }
+      }
+      __syncthreads();
+      // exclusive scan of the chunk popcounts (chunk t)
+      const uint32_t pc = __popc(sM[t]);
+      uint32_t inc = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(FULL, inc, o);
+        if ((int)lane >= o) inc += x;
+      }
+      if (lane == 31) sW[w] = inc;
+      __syncthreads();
+      uint32_t wpre = 0, tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t x = sW[j];
+        wpre += (j < (int)w) ? x : 0u;
+        tot += x;
+      }
+      sO[t] = wpre + inc - pc;
+      __syncthreads();
+      for (int ch = 0; ch < 32; ++ch) {
+        const uint32_t km = sM[32 * w + ch];
+        if ((km >> lane) & 1u)
+          eff[ob + kept + sO[32 * w + ch] + __popc(km & lt_mask)] =
+              __ldg(adj + wb + 32 * ch + lane);
+      }
+      kept += tot;
+      __syncthreads();  // sM / sO / sW reused by the next segment
+    }
+    if (t == 0) edesc[v] = make_desc(ob, kept);
+  }
+  // medium big vertices: one warp each, claimed dynamically
+  const uint64_t nq = c[1];
+  for (;;) {
+    unsigned long long i = 0;
+    if (lane == 0) i = atomicAdd(c + 5, 1ull);
+    i = __shfl_sync(FULL, i, 0);
+    if (i >= nq) break;
     const uint32_t v = bigq[i];
     const uint64_t b = off[v], e = off[v + 1];
     const uint32_t cv = okey<CODED>(deg, dcode, v);
     unsigned long long ob = 0;
-    if (lane == 0) ob = atomicAdd(cursor, (unsigned long long)(e - b));
-    ob = m2 + __shfl_sync(0xffffffffu, ob, 0);
-    uint64_t c = 0;
+    if (lane == 0) ob = atomicAdd(c + 2, (unsigned long long)(e - b));
+    ob = m2 + __shfl_sync(FULL, ob, 0);
+    uint64_t kept = 0;
     for (uint64_t k0 = b; k0 < e; k0 += 32 * kBigU) {
       uint32_t us[kBigU], ks[kBigU];
 #pragma unroll
@@ -511,12 +592,12 @@ k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj
       for (int q = 0; q < kBigU; ++q) {
         const bool keep =
             k0 + 32 * q + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg);
-        const unsigned km = __ballot_sync(0xffffffffu, keep);
-        if (keep) eff[ob + c + __popc(km & lt_mask)] = us[q];
-        c += __popc(km);
+        const unsigned km = __ballot_sync(FULL, keep);
+        if (keep) eff[ob + kept + __popc(km & lt_mask)] = us[q];
+        kept += __popc(km);
       }
     }
-    if (lane == 0) edesc[v] = make_desc(ob, c);
+    if (lane == 0) edesc[v] = make_desc(ob, kept);
   }
 }
 
@@ -790,14 +871,14 @@ static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t ntiles = (g.n + 31) / 32;
   const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
   DBuf<uint32_t> bigq(g.n, s);
-  DBuf<unsigned long long> ctr(3, s);  // tile counter, big-queue size, big-region cursor
+  DBuf<unsigned long long> ctr(6, s);  // tile counter + k_orient_big1's counters
   ctr.zero();
   k_orient_tiles<2, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n,
                                                          nullptr, out.desc.p, out.data.p, ctr.p,
                                                          bigq.p, ctr.p + 1, nullptr, nullptr);
   TG_CHECK_LAUNCH();
-  k_orient_big1<CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p,
-                                               ctr.p + 1, g.m2, ctr.p + 2, out.desc.p, out.data.p);
+  k_orient_big1<CODED><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p, g.n,
+                                               ctr.p, g.m2, out.desc.p, out.data.p);
   TG_CHECK_LAUNCH();
   g_launches += 2;
 }

@@ -266,6 +266,31 @@ def test_long_lists_block_and_global_paths(warp_variant):
             lib().tg_debug_set_block_cap(0)
 
 
+def test_orientation_hubs():
+    """The one-pass orientation's three routes: tile vertices (degree <= 256),
+    warp-per-vertex big vertices (<= 4096) and CTA-per-hub segments of 8192
+    entries (a hub of 20000 spans three), against the oracle's oriented CSR,
+    count and per-node tallies."""
+    rng = np.random.default_rng(5)
+    n = 30000
+    pairs = [(0, v) for v in range(1, 20001)]            # hub, 3 segments
+    pairs += [(1, v) for v in range(2, 5002)]            # hub, 1 segment
+    pairs += [(2, v) for v in range(3, 303)]             # big (warp path)
+    pairs += [(3, v) for v in range(4, 262)]             # just above the tile limit
+    e = rng.integers(0, n, size=(120000, 2))
+    pairs = np.concatenate([np.asarray(pairs, np.int64), e]).astype(np.uint32)
+    ref = O.build_graph(pairs, n)
+    g = T.build_graph(pairs, n)
+    eff = T.effective_adjacency(g)
+    want_off, want_eff = O.effective(ref)
+    assert np.array_equal(eff.offsets, want_off)
+    assert np.array_equal(eff.entries, want_eff)
+    total, tally = O.count(ref, tally=True)[:2]
+    assert T.count_node_iterator_n(g) == total
+    check_against_oracle(g, ref, "seq", 1, "DPD", lists=False)
+    check_against_oracle(g, ref, "aop", 4, "DPD", lists=False)
+
+
 def test_device_step_and_rank_entries():
     import ctypes as C
     import torch
