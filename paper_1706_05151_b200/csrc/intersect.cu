@@ -362,6 +362,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 
 #include "cta.cuh"
 #include "group.cuh"
+#include "quad.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
@@ -370,7 +371,15 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // per 32 lanes: Watts-Strogatz, G(n,m), R-MAT's tail); PA-like lists
   // (h ~ 20) rarely pair up, and the per-apex kernel is faster there.
   const bool groups = g_warp_variant == 0 ? nu.avg_len <= 16.f : g_warp_variant == 2;
-  if (!groups) {  // one apex per warp iteration
+  const bool quads = !WIDE && (g_warp_variant == 0 || g_warp_variant == 3);
+  if (!groups && quads) {  // one apex per warp iteration, quad loads
+    const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kWBlocks);  // resident
+    uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);
+    chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
+    k_intersect_quad<TALLY, LIST, FILTER, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+        (uint32_t)chunk);
+  } else if (!groups) {  // one apex per warp iteration
     const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kWBlocks);  // resident
     uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);   // >= 16 runs per warp
     chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);

@@ -226,7 +226,14 @@ void launch_orient_gappy(const DevGraph& g, uint64_t* desc, uint32_t* eff, cudaS
 //          within a vertex, i.e. exactly the compact EffectiveAdjacency.
 constexpr int kOWarps = 8;
 constexpr int kOTbl = 32;       // table window: 1024 items
-constexpr int kOUnroll = 4;
+#ifndef TG_OUNROLL
+#define TG_OUNROLL 4
+#endif
+#ifndef TG_OBLOCKS
+#define TG_OBLOCKS 5
+#endif
+constexpr int kOUnroll = TG_OUNROLL;
+constexpr int kOBlocks = TG_OBLOCKS;  // resident blocks per SM (launch bounds, grid)
 
 constexpr uint32_t kOBig = 256;  // degree above which a vertex leaves its tile
 constexpr uint32_t kOHub = 4096;  // ... and above which a whole CTA orients it (ONE mode)
@@ -240,7 +247,7 @@ constexpr uint32_t kOHub = 4096;  // ... and above which a whole CTA orients it 
 //          the tile's own adjacency range (ID-sorted, vertex order), no mask,
 //          no scan; big vertices write above m2 (k_orient_big1).
 template <int MODE, bool CODED>
-__global__ void __launch_bounds__(kOWarps * 32, 5)
+__global__ void __launch_bounds__(kOWarps * 32, kOBlocks)
 k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode, uint64_t n,
                uint64_t* __restrict__ cnt_or_eoff,
@@ -817,7 +824,7 @@ void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cud
   TG_CUDA(cudaMemcpyAsync(&ob[1], g.off.p + vhi, 8, cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
   const uint64_t bound = ob[1] - ob[0];  // symmetric entries of the range
-  out.data.alloc(bound ? bound : 1, s);
+  out.data.alloc(bound + kQuadPad, s);
   const uint64_t avg = g.n ? g.m2 / g.n : 0;
   if (avg <= 12) launch_orient<8>(g, vlo, vhi, cnt.p, out.off.p, out.data.p, s);
   else if (avg <= 24) launch_orient<16>(g, vlo, vhi, cnt.p, out.off.p, out.data.p, s);
@@ -836,7 +843,7 @@ void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cud
 template <bool CODED>
 static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t ntiles = (g.n + 31) / 32;
-  const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
+  const unsigned grid = grid_for(ntiles, kOWarps, 148u * kOBlocks);  // resident
   DBuf<uint64_t> cnt(g.n, s);
   DBuf<uint32_t> bigq(g.n, s);
   DBuf<unsigned long long> ctr(3, s);  // tile counters (count, fill), big-queue size
@@ -869,7 +876,7 @@ static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
 template <bool CODED>
 static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t ntiles = (g.n + 31) / 32;
-  const unsigned grid = grid_for(ntiles, kOWarps, 148u * 6u);  // ~resident capacity
+  const unsigned grid = grid_for(ntiles, kOWarps, 148u * kOBlocks);  // resident
   DBuf<uint32_t> bigq(g.n, s);
   DBuf<unsigned long long> ctr(6, s);  // tile counter + k_orient_big1's counters
   ctr.zero();
@@ -898,7 +905,7 @@ void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   out.compact = false;
   out.entries = g.m2 / 2;
   if (out.desc.n < g.n) out.desc.alloc(g.n, s);
-  if (out.data.n < (slots ? slots : 1)) out.data.alloc(slots ? slots : 1, s);
+  if (out.data.n < slots + kQuadPad) out.data.alloc(slots + kQuadPad, s);
   out.off.release();
   if (g.n > (32ull << 20)) orient_onepass<true>(g, out, s);
   else orient_onepass<false>(g, out, s);
@@ -916,7 +923,7 @@ void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s) {
   if (out.off.n < g.n + 1) out.off.alloc(g.n + 1, s);
   // (padding list starts to 32 B was measured: no gain on C2, so lists are
   // packed back to back)
-  if (out.data.n < (m ? m : 1)) out.data.alloc(m ? m : 1, s);
+  if (out.data.n < m + kQuadPad) out.data.alloc(m + kQuadPad, s);
   if (!g.n) {
     TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
     return;
@@ -935,7 +942,7 @@ void orient_full_gappy(const DevGraph& g, DevEff& out, cudaStream_t s) {
   out.compact = false;
   out.entries = g.m2 / 2;
   if (out.desc.n < (g.n ? g.n : 1)) out.desc.alloc(g.n ? g.n : 1, s);
-  if (out.data.n < (g.m2 ? g.m2 : 1)) out.data.alloc(g.m2 ? g.m2 : 1, s);
+  if (out.data.n < g.m2 + kQuadPad) out.data.alloc(g.m2 + kQuadPad, s);
   out.off.release();
   if (!g.n) return;
   const uint64_t avg = g.m2 / g.n;
@@ -952,7 +959,7 @@ void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s) {
   out.entries = in.entries;
   out.off.alloc(rows + 1, s);
   out.desc.alloc(rows ? rows : 1, s);
-  out.data.alloc(in.entries ? in.entries : 1, s);
+  out.data.alloc(in.entries + kQuadPad, s);
   TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
   if (!rows) return;
   DBuf<uint64_t> lens(rows, s);

@@ -126,6 +126,10 @@ struct DevEff {
   DBuf<uint32_t> data;
 };
 
+// List arrays carry kQuadPad extra slots so that the intersection may read
+// the whole 16-byte quad holding a list's last element.
+constexpr uint64_t kQuadPad = 4;
+
 // Read-only view passed to kernels.
 struct CsrView {
   const uint64_t* desc;

@@ -1,8 +1,11 @@
 #!/bin/bash
-# time the C2 intersection pass under each built variant (tools/build_variant.sh)
-cfg=${CFG:-C2}
+# time configs under each built variant (tools/build_variant.sh):
+#   CFGS="C2 C3" tools/variant_sweep.sh
 for d in variants/*/; do
   n=$(basename $d)
-  echo -n "$n "
-  PRE=none TG_LIB_PATH=$PWD/$d/libtrigraph_b200.so python tools/l2_sweep.py $cfg 0 2>&1 | tail -1
+  echo "== $n"
+  TG_LIB_PATH=$PWD/$d/libtrigraph_b200.so python tools/run_configs.py ${CFGS:-C2} --steps 3 2>&1 | grep '^{' | python -c "
+import json,sys
+for l in sys.stdin:
+    r=json.loads(l); print(r['config'], 'orient %.3f'%r['orient_ms'], 'isect %.3f'%r['intersect_ms'], 'T', r['triangles'])"
 done
