@@ -97,6 +97,25 @@ __device__ __forceinline__ uint32_t bm_word(uint32_t h) { return h >> 24; }
 __device__ __forceinline__ uint32_t bm_mask(uint32_t h) {
   return (1u << ((h >> 14) & 31)) | (1u << ((h >> 19) & 31));
 }
+// Quad-kernel variant of the blocked filter, cheaper to probe: stored
+// INVERTED (a cleared bit = present), bit positions from hash bits 0..4 and
+// 5..9 (SHF.L.W takes the amount mod 32), word from the top 8 bits, and the
+// per-warp filter 1 KB-aligned in shared memory so that the word address is
+// base | byte offset.  A probe is IMAD, SHF, LOP3 (address), LDS, SHF, 2x
+// SHF.L.W and one LOP3 that tests (b1 | b2) & word == 0.
+__device__ __forceinline__ uint32_t qm_mask(uint32_t h) {
+  return (1u << (h & 31)) | (1u << ((h >> 5) & 31));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// true iff both bits of x are present; bm = shared address of the filter
+__device__ __forceinline__ bool qm_probe(uint32_t bm, uint32_t x) {
+  const uint32_t h = bm_hash(x);
+  return (qm_mask(h) & lds_u32(bm | ((h >> 22) & 0x3FCu))) == 0u;
+}
 
 // Branch-free membership in an ascending shared-memory array of n <= 64.
 __device__ __forceinline__ bool contains_small(const uint32_t* a, uint32_t n, uint32_t x) {

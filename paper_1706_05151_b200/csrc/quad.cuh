@@ -24,7 +24,7 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                  uint32_t* __restrict__ big, unsigned long long* __restrict__ big_count,
                  uint64_t big_cap, unsigned long long* __restrict__ chunk_ctr, uint32_t chunk) {
   __shared__ uint32_t sNv[kWarpsPerBlock][kWCap];
-  __shared__ uint32_t sBm[kWarpsPerBlock][kBmWords];
+  __shared__ __align__(1024) uint32_t sBm[kWarpsPerBlock][kBmWords];  // inverted filter
   __shared__ uint32_t sTbl[kWarpsPerBlock][kTblWords + kQUnroll + 1];
   __shared__ uint32_t sQs[kWarpsPerBlock][32];  // segment: first quad - first item
   __shared__ uint32_t sHt[kWarpsPerBlock][32];  // segment: head | tail << 2 skipped slots
@@ -39,8 +39,9 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   const uint4* __restrict__ Q4 = reinterpret_cast<const uint4*>(nu.data);
   uint32_t* Nv = sNv[w];
   uint32_t* Bm = sBm[w];
+  const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(Bm);  // 1 KB-aligned
 #pragma unroll
-  for (int i = 0; i < kBmWords / 32; ++i) Bm[lane + 32 * i] = 0;
+  for (int i = 0; i < kBmWords / 32; ++i) Bm[lane + 32 * i] = 0xFFFFFFFFu;
   uint32_t* Tbl = sTbl[w];
   unsigned long long acc = 0;
   __syncwarp();
@@ -75,7 +76,7 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         x = L[i0 + lane];
         Nv[i0 + lane] = x;
         const uint32_t h = bm_hash(x);
-        atomicOr(&Bm[bm_word(h)], bm_mask(h));
+        atomicAnd(&Bm[bm_word(h)], ~qm_mask(h));
       }
       if (FILTER) {
         jlo += __popc(__ballot_sync(FULL, in && x < ulo));
@@ -141,60 +142,57 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         __syncwarp();
         const uint32_t wend = min(S, w0 + 32 * kTblWords);
         for (uint32_t base0 = w0; base0 < wend; base0 += 32 * kQUnroll) {
-          uint32_t xs[kQUnroll][4], jjs[kQUnroll];
-          unsigned valid = 0;  // 4 bits per chunk
+          uint4 r[kQUnroll];
+          uint32_t jjs[kQUnroll];
+#pragma unroll
+          for (int q = 0; q < kQUnroll; ++q) {
+            const uint32_t base = base0 + 32 * q;
+            const uint32_t word = Tbl[(base - w0) >> 5];
+            const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
+            cnt += __popc(word);  // (S's marker only counts past the last item)
+            jjs[q] = jj;
+            const uint32_t qs = __shfl_sync(FULL, my_qs, jj);
+            // lanes past S re-read an in-bounds quad; validity is applied
+            // only on the (rare) exact path below
+            const uint32_t idx = min(base + lane, S - 1);
+            r[q] = __ldg(Q4 + (qs + idx));
+          }
+          // filter over all loaded slots (head/tail slots included)
+          bool p = false;
+#pragma unroll
+          for (int q = 0; q < kQUnroll; ++q)
+            p |= qm_probe(bm_s, r[q].x) | qm_probe(bm_s, r[q].y) | qm_probe(bm_s, r[q].z) |
+                 qm_probe(bm_s, r[q].w);
+          if (!__any_sync(FULL, p)) continue;
+          // exact path: valid slots that pass the filter, branch-free search
+          unsigned fnd = 0;
 #pragma unroll
           for (int q = 0; q < kQUnroll; ++q) {
             const uint32_t base = base0 + 32 * q;
             const uint32_t word = Tbl[(base - w0) >> 5];
             const uint32_t nxt = Tbl[((base - w0) >> 5) + 1];
-            const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
-            cnt += __popc(word);  // (S's marker only counts past the last item)
-            jjs[q] = jj;
-            const uint32_t qs = __shfl_sync(FULL, my_qs, jj);
-            const uint32_t hts = __shfl_sync(FULL, my_ht, jj);
-            const uint32_t idx = base + lane;
-            uint4 r = make_uint4(kNoItem, kNoItem, kNoItem, kNoItem);
-            if (idx < S) r = __ldg(Q4 + (qs + idx));
-            xs[q][0] = r.x;
-            xs[q][1] = r.y;
-            xs[q][2] = r.z;
-            xs[q][3] = r.w;
-            // first quad of a segment drops `head` slots, last drops `tail`
+            const uint32_t hts = __shfl_sync(FULL, my_ht, jjs[q]);
             const bool first = (word >> lane) & 1u;
             const bool last = lane < 31 ? ((word >> (lane + 1)) & 1u) : (nxt & 1u);
-            unsigned vm = idx < S ? 0xFu : 0u;
+            unsigned vm = base + lane < S ? 0xFu : 0u;
             if (first) vm &= (0xFu << (hts & 3u)) & 0xFu;
             if (last) vm &= 0xFu >> (hts >> 2);
-            valid |= vm << (4 * q);
+            const uint32_t xq[4] = {r[q].x, r[q].y, r[q].z, r[q].w};
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+              if (((vm >> s2) & 1u) && qm_probe(bm_s, xq[s2]))
+                fnd |= (unsigned)contains_small(Nv, hv, xq[s2]) << (4 * q + s2);
           }
-          // filter: one LDS.32 per element
-          unsigned hits = 0;
-#pragma unroll
-          for (int q = 0; q < kQUnroll; ++q)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              const uint32_t h = bm_hash(xs[q][s]), bm = bm_mask(h);
-              hits |= (unsigned)((Bm[bm_word(h)] & bm) == bm) << (4 * q + s);
-            }
-          hits &= valid;
-          if (!__any_sync(FULL, hits != 0)) continue;
-          unsigned fnd = 0;
-#pragma unroll
-          for (int q = 0; q < kQUnroll; ++q)
-#pragma unroll
-            for (int s = 0; s < 4; ++s)
-              if ((hits >> (4 * q + s)) & 1u)
-                fnd |= (unsigned)contains_small(Nv, hv, xs[q][s]) << (4 * q + s);
           if (!__any_sync(FULL, fnd != 0)) continue;
           apex_cnt += __popc(fnd);  // per lane; reduced below
           if (TALLY || LIST) {
 #pragma unroll
-            for (int q = 0; q < kQUnroll; ++q)
+            for (int q = 0; q < kQUnroll; ++q) {
+              const uint32_t xq[4] = {r[q].x, r[q].y, r[q].z, r[q].w};
 #pragma unroll
-              for (int s = 0; s < 4; ++s) {
-                const uint32_t x = xs[q][s];
-                const bool found = (fnd >> (4 * q + s)) & 1u;
+              for (int s2 = 0; s2 < 4; ++s2) {
+                const uint32_t x = xq[s2];
+                const bool found = (fnd >> (4 * q + s2)) & 1u;
                 if (TALLY && found) {
                   atomicAdd(&out.tally[x], 1ull);
                   atomicAdd(&sCntU[w][jjs[q]], 1u);
@@ -209,6 +207,7 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                   }
                 }
               }
+            }
           }
         }
         __syncwarp();
@@ -224,7 +223,7 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
     }
     acc += apex_cnt;
     __syncwarp();
-    for (uint32_t i0 = lane; i0 < hv; i0 += 32) Bm[bm_word(bm_hash(Nv[i0]))] = 0;
+    for (uint32_t i0 = lane; i0 < hv; i0 += 32) Bm[bm_word(bm_hash(Nv[i0]))] = 0xFFFFFFFFu;
     __syncwarp();
   }
   unsigned long long a2 = acc;  // per-lane partials
