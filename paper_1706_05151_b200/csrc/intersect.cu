@@ -382,6 +382,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "cta.cuh"
 #include "group.cuh"
 #include "quad.cuh"
+#include "ctaq.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
@@ -428,10 +429,17 @@ void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const Cou
     while ((1u << tl2) < 4u * g_block_cap) ++tl2;
   }
   const int dyn = (int)((1u << tl2) * 4 + (1u << tl2) / 2);  // table + filter (tcap/8 words)
-  TG_CUDA(cudaFuncSetAttribute(k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-  k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex><<<148 * 2, kCT, dyn, s>>>(
-      A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, tl2, scr.big_count.p + 1);
+  if (!WIDE && g_warp_variant != 1) {  // quad loads
+    TG_CUDA(cudaFuncSetAttribute(k_intersect_ctaq<TALLY, LIST, FILTER, Apex>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    k_intersect_ctaq<TALLY, LIST, FILTER, Apex><<<148 * 2, kCT, dyn, s>>>(
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, tl2, scr.big_count.p + 1);
+  } else {
+    TG_CUDA(cudaFuncSetAttribute(k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex><<<148 * 2, kCT, dyn, s>>>(
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, tl2, scr.big_count.p + 1);
+  }
   TG_CHECK_LAUNCH();
   ++g_launches;
 }
