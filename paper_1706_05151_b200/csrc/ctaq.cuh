@@ -163,19 +163,22 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #pragma unroll
           for (int q = 0; q < kCQUnroll; ++q) {
             const uint32_t xq[4] = {r[q].x, r[q].y, r[q].z, r[q].w};
-            // filter, then enqueue the hits (warp-aggregated)
+            // filter (branch-free), then enqueue the hits (warp-aggregated)
+            unsigned hb = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+              const uint32_t h = bm_hash(xq[s2]);
+              hb |= (unsigned)((qm_mask(h) & Bm[h >> wshift]) == 0u) << s2;
+            }
+            hb &= vms[q];
             uint32_t nh = 0;
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
-              const uint32_t x = xq[s2];
-              const uint32_t h = bm_hash(x);
-              const bool hit = ((vms[q] >> s2) & 1u) && (qm_mask(h) & Bm[h >> wshift]) == 0u;
+              const bool hit = (hb >> s2) & 1u;
               const unsigned m = __ballot_sync(FULL, hit);
-              if (hit) {
-                const uint32_t pos = nh + __popc(m & lt_mask);
-                sQx[wid][pos] = x;
-                if (TALLY || LIST) sQj[wid][pos] = jjs[q];
-              }
+              const uint32_t pos = nh + __popc(m & lt_mask);
+              if (hit) sQx[wid][pos] = xq[s2];
+              if ((TALLY || LIST) && hit) sQj[wid][pos] = jjs[q];
               nh += __popc(m);
             }
             __syncwarp();
