@@ -181,9 +181,11 @@ uint64_t tg_kernel_launches(void);
 /* Test hook: shared-memory capacity (entries) of the CTA-path apex staging;
  * lists longer than this are searched in global memory.  0 = default. */
 void tg_debug_set_block_cap(uint32_t entries);
-/* Test hook: warp-path kernel, 0 = automatic (apex groups when the mean
- * oriented list is <= 16 entries, else one apex per warp iteration), 1 = one
- * apex per warp iteration, 2 = apex groups.  All exact. */
+/* Test hook: intersection kernels, 0 = automatic (apex groups when the mean
+ * oriented list is <= 16 entries, else one apex per warp iteration; 16-byte
+ * quad loads when list indices fit 32 bits), 1 = scalar one-apex-per-warp and
+ * scalar CTA path, 2 = quad apex groups, 3 = quad one-apex-per-warp, 4 =
+ * scalar apex groups.  All exact. */
 void tg_debug_set_warp_variant(int32_t variant);
 /* Device-side time (ms) of the last intersection pass (CUDA events on the
  * launching stream); 0 if none. */

@@ -383,6 +383,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "group.cuh"
 #include "quad.cuh"
 #include "ctaq.cuh"
+#include "groupq.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
@@ -390,8 +391,14 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // Apex groups pay off when oriented lists are short (they pack >= 2 apexes
   // per 32 lanes: Watts-Strogatz, G(n,m), R-MAT's tail); PA-like lists
   // (h ~ 20) rarely pair up, and the per-apex kernel is faster there.
-  const bool groups = g_warp_variant == 0 ? nu.avg_len <= 16.f : g_warp_variant == 2;
-  const bool quads = !WIDE && (g_warp_variant == 0 || g_warp_variant == 3);
+  // g_warp_variant: 0 auto, 1 scalar per-apex, 2 groups, 3 quad per-apex,
+  // 4 scalar groups (quads need 32-bit element indices: !WIDE)
+  // Quads waste ~1.5 head/tail slots per list and quantise a group's short
+  // tail; measured: scalar groups win on Watts-Strogatz (mean list 10), quad
+  // groups on R-MAT (15.5), quad per-apex on PA (20).
+  const int wv = g_warp_variant;
+  const bool groups = wv == 0 ? nu.avg_len <= 16.f : (wv == 2 || wv == 4);
+  const bool quads = !WIDE && (wv == 0 ? (!groups || nu.avg_len >= 14.f) : (wv == 2 || wv == 3));
   if (!groups && quads) {  // one apex per warp iteration, quad loads
     const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kWBlocks);  // resident
     uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);
@@ -410,9 +417,14 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
     const unsigned ggrid = grid_for(items, kGWarps * 32, 148u * 5u);
     uint64_t chunk = items / ((uint64_t)ggrid * kGWarps * 8);  // >= 8 chunks per warp
     chunk = chunk < 32 ? 32 : (chunk > 256 ? 256 : chunk);
-    k_intersect_group<TALLY, LIST, FILTER, WIDE, Apex><<<ggrid, kGWarps * 32, 0, s>>>(
-        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
-        (uint32_t)chunk);
+    if (quads)
+      k_intersect_groupq<TALLY, LIST, FILTER, Apex><<<ggrid, kGWarps * 32, 0, s>>>(
+          A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+          (uint32_t)chunk);
+    else
+      k_intersect_group<TALLY, LIST, FILTER, WIDE, Apex><<<ggrid, kGWarps * 32, 0, s>>>(
+          A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+          (uint32_t)chunk);
   }
   TG_CHECK_LAUNCH();
   ++g_launches;
