@@ -358,7 +358,7 @@ def run_ours(args):
     achieved = 4.0 * w_rank / (isect_avg / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": profile_traffic(),
-                "kernel": "intersect pass (k_intersect_warp + k_intersect_block)",
+                "kernel": "intersect pass (k_intersect_quad + k_intersect_ctaq)",
                 "algorithmic_bytes_per_pass": 4 * w_rank, "W": W,
                 "pass_ms": isect_avg, "orient_ms": orient_avg, "peak_source": peak_kind}
 
