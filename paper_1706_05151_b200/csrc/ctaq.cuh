@@ -95,10 +95,10 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         u = L[j];
         const uint64_t d = nu.desc[u - nu.base];
         const uint32_t len = desc_len(d);
-        const uint32_t lo = (uint32_t)desc_start(d), end = lo + len;
-        qs0 = lo >> 2;
-        nq = len ? ((end + 3) >> 2) - qs0 : 0u;
-        ht = (lo & 3u) | (((0u - end) & 3u) << 2);
+        const uint64_t lo = desc_start(d), end = lo + len;  // slots < 2^34
+        qs0 = (uint32_t)(lo >> 2);
+        nq = len ? (uint32_t)(((end + 3) >> 2) - (lo >> 2)) : 0u;
+        ht = ((uint32_t)lo & 3u) | (((0u - (uint32_t)end) & 3u) << 2);
       }
       uint32_t excl, S;
       Scan(scan_tmp).ExclusiveSum(nq, excl, S);

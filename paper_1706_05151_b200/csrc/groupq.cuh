@@ -124,10 +124,10 @@ k_intersect_groupq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         if (!FILTER || (u >= ulo && u < uhi)) {
           const uint64_t d = nu.desc[u - nu.base];
           const uint32_t l = desc_len(d);
-          const uint32_t lo = (uint32_t)desc_start(d), end = lo + l;
-          qs0 = lo >> 2;
-          len = l ? ((end + 3) >> 2) - qs0 : 0u;  // quads
-          ht = (lo & 3u) | (((0u - end) & 3u) << 2);
+          const uint64_t lo = desc_start(d), end = lo + l;  // slots < 2^34
+          qs0 = (uint32_t)(lo >> 2);
+          len = l ? (uint32_t)(((end + 3) >> 2) - (lo >> 2)) : 0u;  // quads
+          ht = ((uint32_t)lo & 3u) | (((0u - (uint32_t)end) & 3u) << 2);
         }
       }
       uint32_t inc2 = len;

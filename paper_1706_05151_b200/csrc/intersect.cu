@@ -398,7 +398,7 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // groups on R-MAT (15.5), quad per-apex on PA (20).
   const int wv = g_warp_variant;
   const bool groups = wv == 0 ? nu.avg_len <= 16.f : (wv == 2 || wv == 4);
-  const bool quads = !WIDE && (wv == 0 ? (!groups || nu.avg_len >= 14.f) : (wv == 2 || wv == 3));
+  const bool quads = nu.quad_ok && (wv == 0 ? (!groups || nu.avg_len >= 14.f) : (wv == 2 || wv == 3));
   if (!groups && quads) {  // one apex per warp iteration, quad loads
     const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kWBlocks);  // resident
     uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);
@@ -441,7 +441,7 @@ void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const Cou
     while ((1u << tl2) < 4u * g_block_cap) ++tl2;
   }
   const int dyn = (int)((1u << tl2) * 4 + (1u << tl2) / 2);  // table + filter (tcap/8 words)
-  if (!WIDE && g_warp_variant != 1) {  // quad loads
+  if (nu.quad_ok && g_warp_variant != 1) {  // quad loads
     TG_CUDA(cudaFuncSetAttribute(k_intersect_ctaq<TALLY, LIST, FILTER, Apex>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     k_intersect_ctaq<TALLY, LIST, FILTER, Apex><<<148 * 2, kCT, dyn, s>>>(
@@ -486,6 +486,7 @@ void dispatch(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t 
               uint64_t data_entries) {
   const bool tally = out.tally != nullptr, list = out.tri != nullptr;
   const bool wide = data_entries >= (1ull << 32);
+  nu.quad_ok = data_entries < (1ull << 34);  // quad indices fit 32 bits
   if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
   else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
   else if (list) launch_pair<false, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);

@@ -894,12 +894,13 @@ static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
 //  * tile layout (default): ONE streaming pass; each tile's lists sit back
 //    to back at the start of the tile's adjacency range, big vertices above
 //    m2 -- list descriptors carry the positions;
-//  * compact layout (when the tile layout would need 64-bit element indices,
-//    > 2^32 slots): count -> CUB scan -> fill, lists back to back.
+//  * compact layout (when the tile layout would exceed 2^34 slots, where the
+//    intersection's 32-bit quad indices end): count -> CUB scan -> fill,
+//    lists back to back.
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
   const uint64_t slots = g.m2 + g.big_entries;
-  if (!g.n || slots >= (1ull << 32)) return orient_full_compact(g, out, s);
+  if (!g.n || slots + kQuadPad >= (1ull << 34)) return orient_full_compact(g, out, s);
   out.rows = g.n;
   out.base = 0;
   out.compact = false;

@@ -136,6 +136,7 @@ struct CsrView {
   const uint32_t* data;
   uint32_t base;
   float avg_len = 0.f;  // host-side hint: mean list length (kernel choice)
+  bool quad_ok = false;  // host-side: list slots < 2^34 (32-bit quad indices)
 };
 
 // ---- build / orient (build.cu, orient.cu) ----
