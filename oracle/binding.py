@@ -52,6 +52,12 @@ def lib():
             "orc_owner": (u64, [vp, u64, C.c_uint32]),
             "orc_run_engine": (u64, [u64, vp, vp, i32, u64, i32, vp, vp, vp, vp, vp,
                                      vp, vp, vp, u64]),
+            "orc_run_engine_ex": (u64, [u64, vp, vp, i32, u64, i32, vp, vp, vp, vp, vp,
+                                        vp, vp, vp, u64, i32, dbl, u64]),
+            "orc_keep_entry": (i32, [dbl, u64, u64, C.c_uint32, C.c_uint32]),
+            "orc_approx_count": (dbl, [u64, vp, vp, u64, i32, dbl, u64, vp, i32]),
+            "orc_per_edge_counts": (None, [u64, vp, vp, vp]),
+            "orc_variance_report": (None, [u64, vp, vp, vp, u64, dbl, vp, vp]),
             "orc_cc": (None, [u64, vp, vp, vp]),
             "orc_random_graph_pairs": (u64, [u64, dbl, u64, vp, u64]),
         }
@@ -98,6 +104,12 @@ def ref():
             "ref_run_engine": (u64, [vp, i32, u64, i32, vp, vp, vp, vp, vp, vp, vp, u64,
                                      vp, i32]),
             "ref_clustering": (i32, [vp, i32, u64, i32, vp, vp]),
+            "ref_run_engine_sparse": (u64, [vp, i32, u64, i32, vp, i32, dbl, u64, vp, vp, vp,
+                                            vp, vp, vp, u64, vp]),
+            "ref_approx_count": (dbl, [vp, u64, i32, dbl, u64, vp, i32]),
+            "ref_keep_entry": (i32, [dbl, u64, i32, u64, C.c_uint32, C.c_uint32]),
+            "ref_per_edge_counts": (u64, [vp, vp]),
+            "ref_variance_report": (None, [vp, vp, u64, dbl, vp, vp]),
             "ref_time_sequential": (dbl, [vp, vp]),
             "ref_prepare": (None, [vp]),
             "ref_aop_sample": (dbl, [vp, u64, vp, u64, i32, vp, vp]),
@@ -201,9 +213,14 @@ class Report:
     triangles_list: np.ndarray | None = None
 
 
+SPARSIFY = {None: 0, "global": 1, "per-partition": 2}
+
+
 def run_engine(g: CSR, engine="aop", ranks=1, cost="DPD", boundaries=None,
-               track_nodes=False, collect_triangles=False) -> Report:
-    """engines.hpp:335-418 run_engine via the C restatement."""
+               track_nodes=False, collect_triangles=False, sparsify=None, q=1.0,
+               seed=0) -> Report:
+    """engines.hpp:335-418 run_engine via the C restatement; sparsify =
+    None | "global" | "per-partition" (SparsifyConfig, sparsify.hpp:22-33)."""
     e = ENGINES[engine]
     p = 1 if engine == "seq" else int(ranks)
     if p == 0:
@@ -215,13 +232,44 @@ def run_engine(g: CSR, engine="aop", ranks=1, cost="DPD", boundaries=None,
     tv = np.zeros(g.n, dtype=U64) if track_nodes else None
     T, _, _ = count(g) if collect_triangles else (0, None, None)
     lst = np.zeros((max(T, 1), 3), dtype=U32) if collect_triangles else None
-    total = L.orc_run_engine(g.n, _ptr(g.off), _ptr(g.adj), e, p, COSTS[cost], _ptr(bi),
-                             _ptr(bo), _ptr(tri), _ptr(sent), _ptr(recv), _ptr(st),
-                             _ptr(tv), _ptr(lst), T)
+    total = L.orc_run_engine_ex(g.n, _ptr(g.off), _ptr(g.adj), e, p, COSTS[cost], _ptr(bi),
+                                _ptr(bo), _ptr(tri), _ptr(sent), _ptr(recv), _ptr(st),
+                                _ptr(tv), _ptr(lst), T, SPARSIFY[sparsify], float(q), int(seed))
     if collect_triangles:
+        T = min(T, int(total))  # sparsified runs list only the kept triangles
         lst = lst[:T]
         lst = lst[np.lexsort((lst[:, 2], lst[:, 1], lst[:, 0]))]
     return Report(int(total), bo, tri, sent, recv, st, tv, lst)
+
+
+def keep_entry(q, seed, rank_key, v, u) -> bool:
+    """sparsify.hpp:58-62 keep_entry (rank key resolved: 0 Global, rank+1
+    PerPartition)."""
+    return bool(lib().orc_keep_entry(float(q), int(seed), int(rank_key), int(v), int(u)))
+
+
+def approx_count(g: CSR, p, engine, q, seed, boundaries=None, cost="DPD") -> float:
+    """engines.hpp:440-457 approx_count."""
+    bi = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=U32)
+    return float(lib().orc_approx_count(g.n, _ptr(g.off), _ptr(g.adj), int(p), ENGINES[engine],
+                                        float(q), int(seed), _ptr(bi), COSTS[cost]))
+
+
+def per_edge_counts(g: CSR) -> np.ndarray:
+    """sequential.hpp:108-122 per_edge_triangle_counts, Graph::edges() order."""
+    te = np.zeros(max(len(g.adj) // 2, 1), dtype=U64)
+    lib().orc_per_edge_counts(g.n, _ptr(g.off), _ptr(g.adj), _ptr(te))
+    return te[: len(g.adj) // 2]
+
+
+def variance_report(g: CSR, boundaries, q):
+    """sparsify.hpp:113-155 variance_report -> (T, k, k', var, var')."""
+    b = np.ascontiguousarray(boundaries, dtype=U32)
+    o3 = np.zeros(3, dtype=U64)
+    v2 = np.zeros(2, dtype=F64)
+    lib().orc_variance_report(g.n, _ptr(g.off), _ptr(g.adj), _ptr(b), len(b) - 1, float(q),
+                              _ptr(o3), _ptr(v2))
+    return int(o3[0]), int(o3[1]), int(o3[2]), float(v2[0]), float(v2[1])
 
 
 def clustering(g: CSR, tv) -> np.ndarray:
@@ -326,6 +374,43 @@ class RefGraph:
             raise ValueError("run_engine: ranks must be >= 1")
         return Report(int(total), bo, tri, sent, recv, np.zeros(p, dtype=U64), tv,
                       None if lst is None else lst[: int(nl[0])])
+
+    def run_engine_sparse(self, engine, ranks, sparsify, q, seed, cost="DPD",
+                          boundaries=None, track_nodes=False, collect_triangles=False):
+        e = ENGINES[engine]
+        p = 1 if engine == "seq" else int(ranks)
+        bo = np.zeros(max(p, 1) + 1, dtype=U32)
+        bi = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=U32)
+        tri, sent, recv = (np.zeros(max(p, 1), dtype=U64) for _ in range(3))
+        tv = np.zeros(self.n, dtype=U64) if track_nodes else None
+        cap = self.count() if collect_triangles else 0
+        lst = np.zeros((max(cap, 1), 3), dtype=U32) if collect_triangles else None
+        nl = np.zeros(1, dtype=U64)
+        total = ref().ref_run_engine_sparse(self.h, e, int(ranks), COSTS[cost], _ptr(bi),
+                                            SPARSIFY[sparsify], float(q), int(seed), _ptr(bo),
+                                            _ptr(tri), _ptr(sent), _ptr(recv), _ptr(tv),
+                                            _ptr(lst), cap, _ptr(nl))
+        if total == 2**64 - 1:
+            raise ValueError("run_engine: invalid arguments")
+        return Report(int(total), bo, tri, sent, recv, np.zeros(p, dtype=U64), tv,
+                      None if lst is None else lst[: int(nl[0])])
+
+    def approx_count(self, p, engine, q, seed, boundaries=None, cost="DPD"):
+        bi = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=U32)
+        return float(ref().ref_approx_count(self.h, int(p), ENGINES[engine], float(q), int(seed),
+                                            _ptr(bi), COSTS[cost]))
+
+    def per_edge_counts(self):
+        te = np.zeros(max(self.m, 1), dtype=U64)
+        k = ref().ref_per_edge_counts(self.h, _ptr(te))
+        return te[:k]
+
+    def variance_report(self, boundaries, q):
+        b = np.ascontiguousarray(boundaries, dtype=U32)
+        o3 = np.zeros(3, dtype=U64)
+        v2 = np.zeros(2, dtype=F64)
+        ref().ref_variance_report(self.h, _ptr(b), len(b) - 1, float(q), _ptr(o3), _ptr(v2))
+        return int(o3[0]), int(o3[1]), int(o3[2]), float(v2[0]), float(v2[1])
 
     def clustering(self, engine="aop", ranks=1, cost="DPD"):
         tv = np.zeros(self.n, dtype=U64)

@@ -207,6 +207,16 @@ static int bsearch_u32(const uint32_t* a, uint64_t n, uint32_t x) {
   return lo < n && a[lo] == x;
 }
 
+static uint64_t lower_bound_u32(const uint32_t* a, uint64_t n, uint32_t x) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint64_t mid = lo + (hi - lo) / 2;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 /* partition.hpp:45-91 node_costs (DpdVariant::EffectiveOnly) + inclusive
  * prefix (:84-89). */
 void orc_node_costs(uint64_t n, const uint64_t* off, const uint32_t* adj,
@@ -360,12 +370,71 @@ static uint64_t surrogate_handle(const effadj_t* E, uint32_t v, const uint32_t* 
   return total;
 }
 
+/* ---- sparsification (sparsify.hpp) ----------------------------------- */
+
+/* sparsify.hpp:37-45 detail::mix64 (the SplitMix64 finaliser). */
+static uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+/* sparsify.hpp:48-54 entry_unit + :58-62 keep_entry, with the rank key
+ * already resolved (0 in Global mode, rank + 1 in PerPartition mode). */
+int orc_keep_entry(double q, uint64_t seed, uint64_t rank_key, uint32_t v, uint32_t u) {
+  uint64_t h = mix64(seed);
+  h = mix64(h ^ rank_key);
+  h = mix64(h ^ ((uint64_t)v + 0x51ed270b684a1571ULL));
+  h = mix64(h ^ (uint64_t)u);
+  return (double)(h >> 11) * 0x1.0p-53 < q;
+}
+
+/* Sparsified copy of E (sparsify.hpp:68-75 sparsify_list per row): row v
+ * keeps entry u iff keep_entry with key kc (b == NULL) or owner(v)+1 (the
+ * non-overlapping partitions of a PerPartition run, sparsify.hpp:85-89). */
+static void sparsify_rows(uint64_t n, const uint64_t* eoff, const uint32_t* eff, double q,
+                          uint64_t seed, uint64_t kc, const uint32_t* b, uint64_t p,
+                          uint64_t* eoff2, uint32_t** eff2) {
+  uint32_t* out = (uint32_t*)malloc((eoff[n] ? eoff[n] : 1) * sizeof(uint32_t));
+  uint64_t w = 0;
+  eoff2[0] = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint64_t key = b ? orc_owner(b, p, (uint32_t)v) + 1 : kc;
+    for (uint64_t k = eoff[v]; k < eoff[v + 1]; ++k)
+      if (orc_keep_entry(q, seed, key, (uint32_t)v, eff[k])) out[w++] = eff[k];
+    eoff2[v + 1] = w;
+  }
+  *eff2 = out;
+}
+
 uint64_t orc_run_engine(uint64_t n, const uint64_t* off, const uint32_t* adj,
                         int engine, uint64_t p, int cost,
                         const uint32_t* boundaries_in, uint32_t* boundaries_out,
                         uint64_t* tri, uint64_t* sent, uint64_t* recv,
                         uint64_t* stored, uint64_t* tally, uint32_t* list,
                         uint64_t list_cap) {
+  return orc_run_engine_ex(n, off, adj, engine, p, cost, boundaries_in, boundaries_out, tri,
+                           sent, recv, stored, tally, list, list_cap, 0, 1.0, 0);
+}
+
+/* engines.hpp:335-418 with cfg.sparsify (smode 1 = Global, 2 =
+ * PerPartition, 0 = none).  Sequential sparsifies the effective adjacency
+ * as rank 0 (:362-365, sparsify.hpp:94-107); AOP sparsifies each rank's
+ * overlap partition with that rank's draws (:367-371, sparsify.hpp:80-84) --
+ * the count equals NodeIteratorN over the apex core on the whole
+ * adjacency sparsified with that key, because N'_v lies inside core+halo;
+ * ANOP sparsifies each rank's core lists with its own draws (:387-391).
+ * stored[] is the partition storage as built (before sparsification). */
+uint64_t orc_run_engine_ex(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                           int engine, uint64_t p, int cost,
+                           const uint32_t* boundaries_in, uint32_t* boundaries_out,
+                           uint64_t* tri, uint64_t* sent, uint64_t* recv,
+                           uint64_t* stored, uint64_t* tally, uint32_t* list,
+                           uint64_t list_cap, int smode, double q, uint64_t seed) {
   /* engines.hpp:337-338 */
   if (engine == ORC_ENGINE_SEQ) p = 1;
   if (p == 0) return UINT64_MAX;
@@ -386,15 +455,40 @@ uint64_t orc_run_engine(uint64_t n, const uint64_t* off, const uint32_t* adj,
   sink_t s = {tally, list, list_cap, 0};
   sink_t* sp = (tally || list) ? &s : NULL;
   for (uint64_t i = 0; i < p; ++i) tri[i] = sent[i] = recv[i] = stored[i] = 0;
+  uint64_t* eoff2 = NULL;
+  uint32_t* eff2 = NULL;
+  if (smode) eoff2 = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
 
   if (engine == ORC_ENGINE_SEQ) {
     /* engines.hpp:362-365 */
-    tri[0] = orc_count(n, eoff, eff, tally, list, list_cap);
     stored[0] = eoff[n];
+    if (smode) {
+      sparsify_rows(n, eoff, eff, q, seed, smode == 2 ? 1 : 0, NULL, 0, eoff2, &eff2);
+      tri[0] = orc_count(n, eoff2, eff2, tally, list, list_cap);
+    } else {
+      tri[0] = orc_count(n, eoff, eff, tally, list, list_cap);
+    }
   } else if (engine == ORC_ENGINE_AOP) {
-    for (uint64_t i = 0; i < p; ++i) tri[i] = aop_rank(&E, b[i], b[i + 1], sp, &stored[i]);
+    for (uint64_t i = 0; i < p; ++i) {
+      if (!smode) {
+        tri[i] = aop_rank(&E, b[i], b[i + 1], sp, &stored[i]);
+        continue;
+      }
+      uint64_t dummy = 0;
+      aop_rank(&E, b[i], b[i + 1], NULL, &stored[i]);
+      sparsify_rows(n, eoff, eff, q, seed, smode == 2 ? i + 1 : 0, NULL, 0, eoff2, &eff2);
+      effadj_t Es = {n, eoff2, eff2};
+      tri[i] = aop_rank(&Es, b[i], b[i + 1], sp, &dummy);
+      free(eff2);
+      eff2 = NULL;
+    }
   } else {
     for (uint64_t i = 0; i < p; ++i) stored[i] = eoff[b[i + 1]] - eoff[b[i]];
+    if (smode) {
+      sparsify_rows(n, eoff, eff, q, seed, 0, smode == 2 ? b : NULL, p, eoff2, &eff2);
+      E.eoff = eoff2;
+      E.eff = eff2;
+    }
     for (uint64_t i = 0; i < p; ++i) {
       uint32_t cb = b[i], ce = b[i + 1];
       for (uint32_t v = cb; v < ce; ++v) {
@@ -432,9 +526,150 @@ uint64_t orc_run_engine(uint64_t n, const uint64_t* off, const uint32_t* adj,
   free(rank);
   free(eoff);
   free(eff);
+  free(eoff2);
+  free(eff2);
   free(f);
   free(prefix);
   return total;
+}
+
+/* engines.hpp:440-457 approx_count: PerPartition draws for AOP, Global for
+ * the others; T' / q^3.  Returns NaN on invalid arguments. */
+double orc_approx_count(uint64_t n, const uint64_t* off, const uint32_t* adj, uint64_t p,
+                        int engine, double q, uint64_t seed, const uint32_t* boundaries,
+                        int cost) {
+  if (!(q > 0.0 && q <= 1.0)) return 0.0 / 0.0; /* sparsify.hpp:28-31 */
+  const uint64_t pp = engine == ORC_ENGINE_SEQ ? 1 : p;
+  if (pp == 0) return 0.0 / 0.0;
+  uint32_t* bo = (uint32_t*)malloc((pp + 1) * sizeof(uint32_t));
+  uint64_t* a = (uint64_t*)malloc(4 * pp * sizeof(uint64_t));
+  const uint64_t t = orc_run_engine_ex(n, off, adj, engine, p, cost, boundaries, bo, a, a + pp,
+                                       a + 2 * pp, a + 3 * pp, NULL, NULL, 0,
+                                       engine == ORC_ENGINE_AOP ? 2 : 1, q, seed);
+  free(bo);
+  free(a);
+  return (double)t / (q * q * q);
+}
+
+/* sequential.hpp:108-122 per_edge_triangle_counts, in Graph::edges() order
+ * (graph.hpp:40-46: u ascending, v ascending, u < v).  te has m entries. */
+void orc_per_edge_counts(uint64_t n, const uint64_t* off, const uint32_t* adj, uint64_t* te) {
+  uint32_t* rank = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  orc_degree_rank(n, off, rank);
+  uint64_t* eoff = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
+  uint32_t* eff = NULL;
+  orc_effective(n, off, adj, rank, eoff, &eff);
+  /* edge index of (a, b), a < b: upper-triangle position */
+  uint64_t* up = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
+  up[0] = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    uint64_t c = 0;
+    for (uint64_t k = off[v]; k < off[v + 1]; ++k) c += adj[k] > v;
+    up[v + 1] = up[v] + c;
+  }
+  memset(te, 0, up[n] * sizeof(uint64_t));
+#define EIDX(a, b) (up[(a)] + lower_bound_u32(adj + off[(a)], off[(a) + 1] - off[(a)], (b)) \
+                    - lower_bound_u32(adj + off[(a)], off[(a) + 1] - off[(a)], (a)))
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint32_t* nv = eff + eoff[v];
+    const uint64_t hv = eoff[v + 1] - eoff[v];
+    for (uint64_t k = 0; k < hv; ++k) {
+      const uint32_t u = nv[k];
+      const uint32_t* nu = eff + eoff[u];
+      const uint64_t hu = eoff[u + 1] - eoff[u];
+      uint64_t i = 0, j = 0;
+      while (i < hv && j < hu) {
+        if (nv[i] < nu[j]) ++i;
+        else if (nu[j] < nv[i]) ++j;
+        else {
+          const uint32_t w = nv[i], x = (uint32_t)v;
+          te[x < u ? EIDX(x, u) : EIDX(u, x)]++;
+          te[x < w ? EIDX(x, w) : EIDX(w, x)]++;
+          te[u < w ? EIDX(u, w) : EIDX(w, u)]++;
+          ++i;
+          ++j;
+        }
+      }
+    }
+  }
+#undef EIDX
+  free(up);
+  free(rank);
+  free(eoff);
+  free(eff);
+}
+
+/* sparsify.hpp:113-155 variance_report: k = pairs of triangles sharing an
+ * edge, k' = those pairs whose apexes (order-smallest corners) have the same
+ * owner under plan b; var = (1/q^3 - 1) T + 2 k (1/q - 1), var' with k'.
+ * out3 = {T, k, k'}, var2 = {var, var'}. */
+void orc_variance_report(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                         const uint32_t* b, uint64_t p, double q, uint64_t* out3,
+                         double* var2) {
+  uint32_t* rank = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  orc_degree_rank(n, off, rank);
+  uint64_t* eoff = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
+  uint32_t* eff = NULL;
+  orc_effective(n, off, adj, rank, eoff, &eff);
+  const uint64_t m = off[n] / 2;
+  /* per edge: count of triangles, and per (edge, owner of apex) counts via
+   * one pass per owner (apexes of core i only) */
+  uint64_t* te = (uint64_t*)malloc((m ? m : 1) * sizeof(uint64_t));
+  uint64_t* up = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
+  up[0] = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    uint64_t c = 0;
+    for (uint64_t k = off[v]; k < off[v + 1]; ++k) c += adj[k] > v;
+    up[v + 1] = up[v] + c;
+  }
+#define EIDX(a, b) (up[(a)] + lower_bound_u32(adj + off[(a)], off[(a) + 1] - off[(a)], (b)) \
+                    - lower_bound_u32(adj + off[(a)], off[(a) + 1] - off[(a)], (a)))
+  uint64_t T = 0, kp = 0;
+  uint64_t* tot = (uint64_t*)calloc(m ? m : 1, sizeof(uint64_t));
+  for (uint64_t i = 0; i < p; ++i) {
+    memset(te, 0, (m ? m : 1) * sizeof(uint64_t));
+    for (uint64_t v = b[i]; v < b[i + 1]; ++v) {
+      const uint32_t* nv = eff + eoff[v];
+      const uint64_t hv = eoff[v + 1] - eoff[v];
+      for (uint64_t k = 0; k < hv; ++k) {
+        const uint32_t u = nv[k];
+        const uint32_t* nu = eff + eoff[u];
+        const uint64_t hu = eoff[u + 1] - eoff[u];
+        uint64_t a = 0, c = 0;
+        while (a < hv && c < hu) {
+          if (nv[a] < nu[c]) ++a;
+          else if (nu[c] < nv[a]) ++c;
+          else {
+            const uint32_t w = nv[a], x = (uint32_t)v;
+            const uint64_t e1 = x < u ? EIDX(x, u) : EIDX(u, x);
+            const uint64_t e2 = x < w ? EIDX(x, w) : EIDX(w, x);
+            const uint64_t e3 = u < w ? EIDX(u, w) : EIDX(w, u);
+            te[e1]++; te[e2]++; te[e3]++;
+            tot[e1]++; tot[e2]++; tot[e3]++;
+            ++T;
+            ++a;
+            ++c;
+          }
+        }
+      }
+    }
+    for (uint64_t e = 0; e < m; ++e) kp += te[e] * (te[e] - (te[e] > 0)) / 2;
+  }
+  uint64_t k = 0;
+  for (uint64_t e = 0; e < m; ++e) k += tot[e] * (tot[e] - (tot[e] > 0)) / 2;
+#undef EIDX
+  out3[0] = T;
+  out3[1] = k;
+  out3[2] = kp;
+  const double q3 = q * q * q;
+  var2[0] = (1.0 / q3 - 1.0) * (double)T + 2.0 * (double)k * (1.0 / q - 1.0);
+  var2[1] = (1.0 / q3 - 1.0) * (double)T + 2.0 * (double)kp * (1.0 / q - 1.0);
+  free(tot);
+  free(te);
+  free(up);
+  free(rank);
+  free(eoff);
+  free(eff);
 }
 
 /* engines.hpp:428-433: C_v = 2 T_v / (d (d-1)) in fp64, 0 when d < 2. */

@@ -85,6 +85,31 @@ uint64_t orc_run_engine(uint64_t n, const uint64_t* off, const uint32_t* adj,
                         uint64_t* stored, uint64_t* tally, uint32_t* list,
                         uint64_t list_cap);
 
+/* orc_run_engine with cfg.sparsify (engines.hpp:279, sparsify.hpp):
+ * smode 0 = none, 1 = Global, 2 = PerPartition; q in (0, 1]. */
+uint64_t orc_run_engine_ex(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                           int engine, uint64_t p, int cost,
+                           const uint32_t* boundaries_in, uint32_t* boundaries_out,
+                           uint64_t* tri, uint64_t* sent, uint64_t* recv,
+                           uint64_t* stored, uint64_t* tally, uint32_t* list,
+                           uint64_t list_cap, int smode, double q, uint64_t seed);
+
+/* sparsify.hpp:58-62 keep_entry with a resolved rank key. */
+int orc_keep_entry(double q, uint64_t seed, uint64_t rank_key, uint32_t v, uint32_t u);
+
+/* engines.hpp:440-457 approx_count (T' / q^3). */
+double orc_approx_count(uint64_t n, const uint64_t* off, const uint32_t* adj, uint64_t p,
+                        int engine, double q, uint64_t seed, const uint32_t* boundaries,
+                        int cost);
+
+/* sequential.hpp:108-122 per_edge_triangle_counts in Graph::edges() order. */
+void orc_per_edge_counts(uint64_t n, const uint64_t* off, const uint32_t* adj, uint64_t* te);
+
+/* sparsify.hpp:113-155 variance_report: out3 = {T, k, k'}, var2 = {var, var'}. */
+void orc_variance_report(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                         const uint32_t* b, uint64_t p, double q, uint64_t* out3,
+                         double* var2);
+
 /* engines.hpp:422-435 clustering coefficient formula. */
 void orc_cc(uint64_t n, const uint64_t* off, const uint64_t* tally, double* c);
 

@@ -194,6 +194,88 @@ uint64_t ref_run_engine(void* h, int engine, uint64_t p, int cost, const uint32_
   return rep.total;
 }
 
+// run_engine with cfg.sparsify (smode 1 = Global, 2 = PerPartition)
+uint64_t ref_run_engine_sparse(void* h, int engine, uint64_t p, int cost, const uint32_t* b_in,
+                               int smode, double q, uint64_t seed, uint32_t* b_out, uint64_t* tri,
+                               uint64_t* sent, uint64_t* recv, uint64_t* tally, uint32_t* list,
+                               uint64_t cap, uint64_t* n_listed) {
+  auto* r = static_cast<RefGraph*>(h);
+  EngineConfig cfg;
+  cfg.engine = static_cast<EngineKind>(engine);
+  cfg.ranks = p;
+  cfg.cost = static_cast<CostKind>(cost);
+  cfg.track_nodes = tally != nullptr;
+  cfg.collect_triangles = list != nullptr;
+  cfg.sparsify = SparsifyConfig{q, seed,
+                                smode == 2 ? SparsifyConfig::Mode::PerPartition
+                                           : SparsifyConfig::Mode::Global};
+  uint64_t pp = cfg.engine == EngineKind::Sequential ? 1 : p;
+  if (b_in) cfg.boundaries = std::vector<NodeId>(b_in, b_in + pp + 1);
+  RunReport rep;
+  try {
+    rep = run_engine(r->g, cfg);
+  } catch (const std::invalid_argument&) {
+    return UINT64_MAX;
+  }
+  std::memcpy(b_out, rep.boundaries.data(), rep.boundaries.size() * sizeof(uint32_t));
+  for (std::size_t i = 0; i < rep.per_rank.size(); ++i) {
+    tri[i] = rep.per_rank[i].triangles;
+    sent[i] = rep.per_rank[i].data_sent;
+    recv[i] = rep.per_rank[i].data_recv;
+  }
+  if (tally)
+    std::memcpy(tally, rep.node_counts.data(), rep.node_counts.size() * sizeof(uint64_t));
+  if (list) {
+    std::sort(rep.triangles_list.begin(), rep.triangles_list.end());
+    *n_listed = rep.triangles_list.size();
+    for (uint64_t k = 0; k < rep.triangles_list.size() && k < cap; ++k)
+      for (int c = 0; c < 3; ++c) list[3 * k + c] = rep.triangles_list[k][c];
+  }
+  return rep.total;
+}
+
+double ref_approx_count(void* h, uint64_t p, int engine, double q, uint64_t seed,
+                        const uint32_t* b_in, int cost) {
+  auto* r = static_cast<RefGraph*>(h);
+  std::optional<std::vector<NodeId>> b;
+  uint64_t pp = static_cast<EngineKind>(engine) == EngineKind::Sequential ? 1 : p;
+  if (b_in) b = std::vector<NodeId>(b_in, b_in + pp + 1);
+  try {
+    return approx_count(r->g, p, static_cast<EngineKind>(engine), q, seed,
+                        runtime::ExecMode::Interleaved, b, static_cast<CostKind>(cost));
+  } catch (const std::invalid_argument&) {
+    return std::nan("");
+  }
+}
+
+int ref_keep_entry(double q, uint64_t seed, int smode, uint64_t rank, uint32_t v, uint32_t u) {
+  SparsifyConfig cfg{q, seed,
+                     smode == 2 ? SparsifyConfig::Mode::PerPartition : SparsifyConfig::Mode::Global};
+  return keep_entry(cfg, rank, v, u) ? 1 : 0;
+}
+
+// per_edge_triangle_counts (sequential.hpp:108-122) in Graph::edges() order
+uint64_t ref_per_edge_counts(void* h, uint64_t* te) {
+  auto* r = static_cast<RefGraph*>(h);
+  auto& eff = r->effective();
+  auto m = per_edge_triangle_counts(r->g, eff);
+  uint64_t k = 0;
+  for (auto [u, v] : r->g.edges()) te[k++] = m.at({u, v});
+  return k;
+}
+
+void ref_variance_report(void* h, const uint32_t* b, uint64_t p, double q, uint64_t* out3,
+                         double* var2) {
+  auto* r = static_cast<RefGraph*>(h);
+  PartitionPlan plan{std::vector<NodeId>(b, b + p + 1)};
+  auto rep = variance_report(r->g, plan, q);
+  out3[0] = rep.triangles;
+  out3[1] = rep.k;
+  out3[2] = rep.k_prime;
+  var2[0] = rep.var;
+  var2[1] = rep.var_prime;
+}
+
 int ref_clustering(void* h, int engine, uint64_t p, int cost, uint64_t* tally, double* c) {
   auto* r = static_cast<RefGraph*>(h);
   EngineConfig cfg;

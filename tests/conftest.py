@@ -44,3 +44,10 @@ def full_golden():
         pytest.skip("reference_full.json not generated")
     with open(p) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def next_golden():
+    """sparsification, per-edge counts, variance report."""
+    with open(os.path.join(GOLDEN, "reference_next.json")) as f:
+        return json.load(f)

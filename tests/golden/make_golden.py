@@ -4,6 +4,7 @@ Run here (where /root/reference is mounted and `make -C oracle` built
 oracle/_ref/libtrigraph_ref.so):
 
     python tests/golden/make_golden.py            # small fixtures (seconds)
+    python tests/golden/make_golden.py --next     # only the 8(f) rows (sparsify, t_e)
     python tests/golden/make_golden.py --full     # + full-size C1/C2 goldens
 
 Every number in the fixtures comes from the reference's own functions
@@ -152,6 +153,68 @@ def small():
     return fx
 
 
+def sparse_record(R: B.RefGraph, engine, p, mode, q, seed):
+    rep = R.run_engine_sparse(engine, p, mode, q, seed, track_nodes=True, collect_triangles=True)
+    pp = 1 if engine == "seq" else p
+    return {
+        "engine": engine, "ranks": p, "sparsify": mode, "q": q, "seed": seed,
+        "total": rep.total,
+        "triangles": rep.triangles[:pp].tolist(),
+        "data_sent": rep.data_sent[:pp].tolist(),
+        "data_recv": rep.data_recv[:pp].tolist(),
+        "node_counts_sha256": digest(rep.node_counts),
+        "triangles_sha256": digest(rep.triangles_list),
+    }
+
+
+def next_rows():
+    """sparsification (sparsify.hpp, engines.hpp:440-457),
+    per-edge triangle counts (sequential.hpp:108-122), variance_report."""
+    fx = {}
+    rng = np.random.default_rng(1706)
+    keep = []
+    for _ in range(256):
+        q = float(rng.choice([0.1, 0.25, 0.5, 0.9, 1.0]))
+        seed = int(rng.integers(1 << 63))
+        mode = int(rng.integers(1, 3))
+        rank = int(rng.integers(0, 16))
+        v, u = (int(x) for x in rng.integers(0, 1 << 32, size=2))
+        keep.append([q, seed, mode, rank, v, u, int(B.ref().ref_keep_entry(q, seed, mode, rank, v,
+                                                                          u))])
+    fx["keep_entry"] = keep
+    graphs = [("pa20000", B.ref_fixture("gen_pa", 20000, 20, 3))]
+    for i, (n, dens, seed) in enumerate(((60, 0.3, 11), (90, 0.5, 12), (40, 0.8, 13))):
+        graphs.append((f"random{i}", B.ref_random_graph(n, dens, seed)))
+    recs = {}
+    for name, R in graphs:
+        g = R.csr()
+        te = R.per_edge_counts()
+        rec = {"n": g.n, "m": g.m, "adj_sha256": digest(g.adj),
+               "per_edge_sha256": digest(te), "per_edge_sum": int(te.sum()),
+               "k": int(sum(int(c) * (int(c) - 1) // 2 for c in te))}
+        if name != "pa20000":
+            rec["per_edge"] = te.tolist()
+        rec["sparse"] = [sparse_record(R, e, p, mode, q, 77 + p)
+                         for e in ENGINES for mode in ("global", "per-partition")
+                         for (p, q) in ((1, 0.5), (3, 0.5), (4, 0.25), (8, 0.7))
+                         if not (e == "seq" and p > 1)]
+        rec["approx"] = [{"engine": e, "ranks": p, "q": q, "seed": 5,
+                          "value": float(R.approx_count(p, e, q, 5)).hex()}
+                         for e in ENGINES for (p, q) in ((1, 0.5), (4, 0.3))]
+        pre = R.node_costs("DPD")[1]
+        f = R.node_costs("DPD")[0]
+        rec["variance"] = []
+        for p in (2, 4, 8):
+            b = np.zeros(p + 1, dtype=np.uint32)
+            B.ref().ref_compute_boundaries(f.ctypes.data, len(f), p, b.ctypes.data)
+            T, k, kp, var, varp = R.variance_report(b, 0.5)
+            rec["variance"].append({"boundaries": b.tolist(), "q": 0.5, "T": T, "k": k,
+                                    "k_prime": kp, "var": var.hex(), "var_prime": varp.hex()})
+        recs[name] = rec
+    fx["graphs"] = recs
+    return fx
+
+
 def full():
     sys.path.insert(0, ROOT)
     from paper_1706_05151_b200 import trigraph as T  # generators only (host harness)
@@ -180,9 +243,16 @@ def full():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", action="store_true")
+    ap.add_argument("--next", action="store_true", help="only reference_next.json")
     a = ap.parse_args()
     if not B.ref_available():
         sys.exit("oracle/_ref not built (make -C oracle with /root/reference mounted)")
+    fx = next_rows()
+    with open(os.path.join(OUT, "reference_next.json"), "w") as f:
+        json.dump(fx, f, indent=0, sort_keys=True)
+    print("wrote reference_next.json")
+    if a.next:
+        sys.exit(0)
     fx = small()
     with open(os.path.join(OUT, "reference_small.json"), "w") as f:
         json.dump(fx, f, indent=0, sort_keys=True)
