@@ -70,7 +70,15 @@ typedef struct {
   const uint32_t* boundaries;/* optional override, ranks+1 entries, host memory */
   int32_t track_nodes;       /* fill per-node counts */
   int32_t collect_triangles; /* fill the triangle list */
+  /* optional<SparsifyConfig> (engines.hpp:279, sparsify.hpp:22-33):
+   * TG_SPARSIFY_NONE / _GLOBAL / _PER_PARTITION, retention q in (0, 1]. */
+  int32_t sparsify;
+  double sparsify_q;
+  uint64_t sparsify_seed;
 } tg_config;
+
+/* sparsify.hpp:22-24 SparsifyConfig::Mode (0 = no sparsification). */
+typedef enum { TG_SPARSIFY_NONE = 0, TG_SPARSIFY_GLOBAL = 1, TG_SPARSIFY_PER_PARTITION = 2 } tg_sparsify;
 
 /* engines.hpp:282-287 RankStats.  realized_cost is reported as the
  * algorithmic work sum_{v->u in rank} (h_v + h_u) (the DPD cost of the rank's
@@ -139,6 +147,23 @@ tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total,
 /* clustering_coefficients(g, cfg) (engines.hpp:422-435): T_v (n) and C_v (n). */
 tg_status tg_clustering_coefficients(tg_graph* g, const tg_config* cfg,
                                      uint64_t* triangles_per_node, double* coefficient);
+
+/* ---- approximate counting and per-edge analytics ---- */
+
+/* approx_count(g, p, engine, q, seed, boundaries, cost) (engines.hpp:440-457):
+ * sparsify-then-count estimate T' / q^3, PerPartition draws for AOP and
+ * Global draws otherwise.  boundaries: optional (p+1 entries, host). */
+tg_status tg_approx_count(tg_graph* g, uint64_t p, int32_t engine, double q, uint64_t seed,
+                          const uint32_t* boundaries, int32_t cost, double* estimate);
+/* per_edge_triangle_counts(g, eff) (sequential.hpp:108-122): t_e for every
+ * edge in Graph::edges() order (u < v, u then v ascending; graph.hpp:40-46);
+ * te has num_edges entries (host or device memory). */
+tg_status tg_per_edge_triangle_counts(tg_graph* g, uint64_t* te);
+/* variance_report(g, plan, q) (sparsify.hpp:113-155): out3 = {T, k, k'},
+ * var2 = {var, var'} for the 1/q^3-scaled estimator under the plan given by
+ * `boundaries` (p+1 entries, host). */
+tg_status tg_variance_report(tg_graph* g, const uint32_t* boundaries, uint64_t p, double q,
+                             uint64_t* out3, double* var2);
 
 /* ---- device-resident hot path (bench / multi-process drivers) ---- */
 

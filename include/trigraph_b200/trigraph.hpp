@@ -18,6 +18,7 @@
 #include <array>
 #include <cstddef>
 #include <cstdint>
+#include <map>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -187,6 +188,17 @@ inline PartitionPlan compute_boundaries(const Graph& g, CostKind kind, std::size
   return plan;
 }
 
+/// sparsify.hpp:22-33.
+struct SparsifyConfig {
+  enum class Mode { PerPartition, Global };
+  double q = 1.0;
+  std::uint64_t seed = 0;
+  Mode mode = Mode::Global;
+  void validate() const {
+    if (!(q > 0.0 && q <= 1.0)) throw std::invalid_argument("sparsify: q must be in (0, 1]");
+  }
+};
+
 /// engines.hpp:270-298.
 struct EngineConfig {
   EngineKind engine = EngineKind::Aop;
@@ -195,6 +207,7 @@ struct EngineConfig {
   runtime::ExecMode mode = runtime::ExecMode::Interleaved;
   bool track_nodes = false;
   bool collect_triangles = false;
+  std::optional<SparsifyConfig> sparsify;
   std::optional<std::vector<NodeId>> boundaries;
 };
 
@@ -223,6 +236,14 @@ inline tg_config to_c(const EngineConfig& cfg) {
   c.boundaries = cfg.boundaries ? cfg.boundaries->data() : nullptr;
   c.track_nodes = cfg.track_nodes;
   c.collect_triangles = cfg.collect_triangles;
+  if (cfg.sparsify) {
+    cfg.sparsify->validate();
+    c.sparsify = cfg.sparsify->mode == SparsifyConfig::Mode::PerPartition
+                     ? TG_SPARSIFY_PER_PARTITION
+                     : TG_SPARSIFY_GLOBAL;
+    c.sparsify_q = cfg.sparsify->q;
+    c.sparsify_seed = cfg.sparsify->seed;
+  }
   return c;
 }
 }  // namespace detail
@@ -273,6 +294,46 @@ inline ClusteringResult clustering_coefficients(const Graph& g, EngineConfig cfg
   detail::check(tg_clustering_coefficients(g.handle(), &c, r.triangles_per_node.data(),
                                            r.coefficient.data()));
   return r;
+}
+
+/// engines.hpp:440-457 approx_count: T' / q^3 (AOP: per-partition draws).
+inline double approx_count(const Graph& g, std::size_t p, EngineKind engine, double q,
+                           std::uint64_t seed,
+                           runtime::ExecMode = runtime::ExecMode::Interleaved,
+                           const std::optional<std::vector<NodeId>>& boundaries = {},
+                           CostKind cost = CostKind::Dpd) {
+  double est = 0.0;
+  detail::check(tg_approx_count(g.handle(), p, static_cast<int32_t>(engine), q, seed,
+                                boundaries ? boundaries->data() : nullptr,
+                                static_cast<int32_t>(cost), &est));
+  return est;
+}
+
+/// sequential.hpp:108-122 per_edge_triangle_counts, keyed like the
+/// reference's map by the (u < v) edge pairs in Graph::edges() order.
+inline std::map<std::pair<NodeId, NodeId>, std::uint64_t> per_edge_triangle_counts(
+    const Graph& g) {
+  std::vector<std::uint64_t> te(g.num_edges());
+  detail::check(tg_per_edge_triangle_counts(g.handle(), te.data()));
+  std::map<std::pair<NodeId, NodeId>, std::uint64_t> out;
+  const auto [off, adj] = g.csr();
+  std::uint64_t k = 0;
+  for (NodeId u = 0; u + 1 < off.size(); ++u)
+    for (std::uint64_t i = off[u]; i < off[u + 1]; ++i)
+      if (u < adj[i]) out[{u, adj[i]}] = te[k++];
+  return out;
+}
+
+/// sparsify.hpp:113-155 variance_report.
+struct VarianceReport {
+  std::uint64_t triangles = 0, k = 0, k_prime = 0;
+  double q = 1.0, var = 0.0, var_prime = 0.0;
+};
+inline VarianceReport variance_report(const Graph& g, const PartitionPlan& plan, double q) {
+  std::uint64_t o3[3];
+  double v2[2];
+  detail::check(tg_variance_report(g.handle(), plan.boundaries.data(), plan.ranks(), q, o3, v2));
+  return {o3[0], o3[1], o3[2], q, v2[0], v2[1]};
 }
 
 /// io.hpp:129-162 gen_pa (host, bit-identical edge stream).

@@ -29,6 +29,9 @@ class TgConfig(C.Structure):
         ("boundaries", C.c_void_p),
         ("track_nodes", C.c_int32),
         ("collect_triangles", C.c_int32),
+        ("sparsify", C.c_int32),
+        ("sparsify_q", C.c_double),
+        ("sparsify_seed", C.c_uint64),
     ]
 
 
@@ -60,6 +63,9 @@ SIGNATURES = {
     "tg_count": (_i32, [_vp, _pu64]),
     "tg_run_engine": (_i32, [_vp, C.POINTER(TgConfig), _pu64, _vp, _vp, _vp, _vp, _u64, _pu64]),
     "tg_clustering_coefficients": (_i32, [_vp, C.POINTER(TgConfig), _vp, _vp]),
+    "tg_approx_count": (_i32, [_vp, _u64, _i32, _dbl, _u64, _vp, _i32, C.POINTER(_dbl)]),
+    "tg_per_edge_triangle_counts": (_i32, [_vp, _vp]),
+    "tg_variance_report": (_i32, [_vp, _vp, _u64, _dbl, _vp, _vp]),
     "tg_step_device": (_i32, [_vp, _vp]),
     "tg_orient_device": (_i32, [_vp]),
     "tg_count_device": (_i32, [_vp, _vp]),

@@ -206,24 +206,61 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
   };
   const CsrView full = view(g->eff);
   const uint32_t N = (uint32_t)n;
+  // sparsify.hpp: the engines below count over sparsified lists; partition
+  // storage (stored_entries) is reported as built, before sparsification
+  const int sp = cfg.sparsify;
+  TG_REQUIRE(sp >= TG_SPARSIFY_NONE && sp <= TG_SPARSIFY_PER_PARTITION, "unknown sparsify mode");
+  if (sp) TG_REQUIRE(cfg.sparsify_q > 0.0 && cfg.sparsify_q <= 1.0, "sparsify: q must be in (0, 1]");
+  const double sq = cfg.sparsify_q;
+  const uint64_t sseed = cfg.sparsify_seed;
+  DBuf<uint32_t> d_b;
+  if (sp == TG_SPARSIFY_PER_PARTITION && cfg.engine == TG_ENGINE_ANOP_DIRECT)
+    upload(d_b, b.data(), b.size(), s);
 
   if (cfg.engine == TG_ENGINE_SEQ) {
-    timed_pass(g, [&] { tgb::intersect_rows(full, 0, N, full, 0, N, out_for(0), g->scr, s, g->eff.data.n, true);
+    // engines.hpp:362-365 / sparsify.hpp:94-107: rank 0's draws
+    DevEff es;
+    if (sp) tgb::sparsify_eff(g->eff, es, sq, sseed, sp == TG_SPARSIFY_PER_PARTITION ? 1 : 0,
+                              nullptr, 0, s);
+    const DevEff& E = sp ? es : g->eff;
+    const CsrView ev = view(E);
+    timed_pass(g, [&] { tgb::intersect_rows(ev, 0, N, ev, 0, N, out_for(0), g->scr, s, E.data.n, true);
     });
     R.per_rank[0].stored_entries = g->eff.entries;
+  } else if (sp && cfg.engine == TG_ENGINE_AOP) {
+    // engines.hpp:367-371 + sparsify.hpp:80-84: each rank sparsifies its
+    // overlap partition with its own draws; N'_v lies in core+halo, so the
+    // rank's count is NodeIteratorN over its apexes on the adjacency
+    // sparsified with its key
+    DevEff es;
+    if (sp == TG_SPARSIFY_GLOBAL) tgb::sparsify_eff(g->eff, es, sq, sseed, 0, nullptr, 0, s);
+    for (uint64_t i = 0; i < p; ++i) {
+      if (sp == TG_SPARSIFY_PER_PARTITION) tgb::sparsify_eff(g->eff, es, sq, sseed, i + 1, nullptr, 0, s);
+      const CsrView ev = view(es);
+      if (b[i + 1] > b[i])
+        tgb::intersect_rows(ev, b[i], b[i + 1], ev, 0, N, out_for(i), g->scr, s, es.data.n, true);
+      R.per_rank[i].stored_entries = tgb::overlap_stored_entries(full, n, b[i], b[i + 1], s);
+    }
   } else if (cfg.engine == TG_ENGINE_AOP || cfg.engine == TG_ENGINE_ANOP_DIRECT) {
+    // direct (engines.hpp:80-141): every rank's core lists with its own
+    // draws (owner key), then the same requests over the kept entries
+    DevEff es;
+    if (sp) tgb::sparsify_eff(g->eff, es, sq, sseed, 0,
+                              sp == TG_SPARSIFY_PER_PARTITION ? d_b.p : nullptr, p, s);
+    const DevEff& E = sp ? es : g->eff;
+    const CsrView ev = view(E);
     timed_pass(g, [&] {
       for (uint64_t i = 0; i < p; ++i)
         if (b[i + 1] > b[i])
-          tgb::intersect_rows(full, b[i], b[i + 1], full, 0, N, out_for(i), g->scr, s,
-                              g->eff.data.n, true);
+          tgb::intersect_rows(ev, b[i], b[i + 1], ev, 0, N, out_for(i), g->scr, s,
+                              E.data.n, true);
     });
     if (cfg.engine == TG_ENGINE_AOP) {
       for (uint64_t i = 0; i < p; ++i)
         R.per_rank[i].stored_entries = tgb::overlap_stored_entries(full, n, b[i], b[i + 1], s);
     } else {
       std::vector<uint64_t> req, rep;
-      tgb::direct_messages(full, n, b, req, rep, s);
+      tgb::direct_messages(ev, n, b, req, rep, s);
       for (uint64_t i = 0; i < p; ++i) {
         R.per_rank[i].data_sent = req[i] + rep[i];
         R.per_rank[i].data_recv = req[i] + rep[i];
@@ -238,6 +275,12 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
     for (uint64_t i = 0; i < p; ++i) {
       tgb::orient_rows(g->g, b[i], b[i + 1], parts[i], s);  // non-overlapping storage
       R.per_rank[i].stored_entries = parts[i].entries;
+      if (sp) {  // sparsify.hpp:86-90: the rank's core lists, its own draws
+        DevEff es;
+        tgb::sparsify_eff(parts[i], es, sq, sseed, sp == TG_SPARSIFY_PER_PARTITION ? i + 1 : 0,
+                          nullptr, 0, s);
+        parts[i] = std::move(es);
+      }
       packs[i].build(view(parts[i]), b[i], b[i + 1], b, (uint32_t)i, s);
       uint64_t msgs = 0, words = 0;
       for (uint64_t j = 0; j < p; ++j) {
@@ -334,6 +377,42 @@ void prepare_part(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t 
   g->part_rank = rank;
   g->have_part = true;
 }
+
+}  // namespace
+
+namespace {
+
+// NodeIteratorN listing of apexes [lo, hi) in pieces whose triangles fit the
+// buffer (count first; halve the apex range while it holds too many).
+template <class F>
+void list_in_pieces(tg_graph* g, uint32_t lo, uint32_t hi, DBuf<uint32_t>& tri, uint64_t cap,
+                    F&& f) {
+  if (hi <= lo) return;
+  cudaStream_t s = g->stream;
+  const CsrView full = view(g->eff);
+  const uint32_t N = (uint32_t)g->g.n;
+  DBuf<unsigned long long> c(2, s);
+  c.zero();
+  tgb::intersect_rows(full, lo, hi, full, 0, N, CountOut{c.p, nullptr, nullptr, nullptr, 0},
+                      g->scr, s, g->eff.data.n, true);
+  unsigned long long cnt = 0;
+  download(&cnt, c.p, 1, s);
+  sync(g);
+  if (!cnt) return;
+  if (cnt > cap && hi - lo > 1) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    list_in_pieces(g, lo, mid, tri, cap, f);
+    list_in_pieces(g, mid, hi, tri, cap, f);
+    return;
+  }
+  TG_REQUIRE(cnt <= cap, "one apex has more triangles than the listing buffer");
+  c.zero();
+  tgb::intersect_rows(full, lo, hi, full, 0, N, CountOut{c.p, nullptr, tri.p, c.p + 1, cap},
+                      g->scr, s, g->eff.data.n, true);
+  f(tri.p, (uint64_t)cnt);
+}
+
+constexpr uint64_t kListCap = 1ull << 26;  // triples per listing piece (768 MB)
 
 }  // namespace
 
@@ -563,6 +642,89 @@ tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total, tg_r
     return cap_status;
   }
   return st;
+}
+
+tg_status tg_approx_count(tg_graph* g, uint64_t p, int32_t engine, double q, uint64_t seed,
+                          const uint32_t* boundaries, int32_t cost, double* estimate) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(estimate != nullptr, "null output");
+    TG_REQUIRE(q > 0.0 && q <= 1.0, "sparsify: q must be in (0, 1]");  // sparsify.hpp:28-31
+    tg_config c{};
+    c.engine = engine;
+    c.cost = cost;
+    c.ranks = p;
+    c.boundaries = boundaries;
+    // engines.hpp:450-452: per-partition draws for AOP, one draw per edge otherwise
+    c.sparsify = engine == TG_ENGINE_AOP ? TG_SPARSIFY_PER_PARTITION : TG_SPARSIFY_GLOBAL;
+    c.sparsify_q = q;
+    c.sparsify_seed = seed;
+    EngineResult R = run(g, c, nullptr, nullptr, nullptr, 0);
+    *estimate = (double)R.total / (q * q * q);
+  });
+}
+
+tg_status tg_per_edge_triangle_counts(tg_graph* g, uint64_t* te) {
+  return guard([&] {
+    enter(g);
+    cudaStream_t s = g->stream;
+    ensure_eff(g);
+    const uint64_t n = g->g.n, m = g->g.m2 / 2;
+    TG_REQUIRE(te != nullptr || m == 0, "null output");
+    if (!m) return;
+    DBuf<uint64_t> up(n + 1, s);
+    tgb::upper_offsets(g->g, up.p, s);
+    DBuf<unsigned long long> dte(m, s);
+    dte.zero();
+    const uint64_t T = seq_count(g);
+    const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(T, kListCap));
+    DBuf<uint32_t> tri(3 * cap, s);
+    list_in_pieces(g, 0, (uint32_t)n, tri, cap, [&](const uint32_t* t, uint64_t cnt) {
+      tgb::bump_edges(g->g, up.p, t, cnt, dte.p, nullptr, s);
+    });
+    TG_CUDA(cudaMemcpyAsync(te, dte.p, m * 8, is_device_ptr(te) ? cudaMemcpyDeviceToDevice
+                                                                : cudaMemcpyDeviceToHost, s));
+    sync(g);
+  });
+}
+
+tg_status tg_variance_report(tg_graph* g, const uint32_t* boundaries, uint64_t p, double q,
+                             uint64_t* out3, double* var2) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(boundaries && p >= 1 && out3 && var2, "invalid argument");
+    cudaStream_t s = g->stream;
+    ensure_eff(g);
+    const std::vector<uint32_t> b = plan_for(g, TG_COST_DPD, p, boundaries);
+    const uint64_t n = g->g.n, m = g->g.m2 / 2;
+    uint64_t T = 0, k = 0, kp = 0;
+    if (m) {
+      DBuf<uint64_t> up(n + 1, s);
+      tgb::upper_offsets(g->g, up.p, s);
+      DBuf<unsigned long long> tot(m, s), per(m, s);
+      tot.zero();
+      const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(seq_count(g), kListCap));
+      DBuf<uint32_t> tri(3 * cap, s);
+      // k' (sparsify.hpp:140-144): pairs of triangles on one edge whose
+      // apexes share an owner = sum over ranks of the pairs among the
+      // triangles with apex in that core
+      for (uint64_t i = 0; i < p; ++i) {
+        per.zero();
+        list_in_pieces(g, b[i], b[i + 1], tri, cap, [&](const uint32_t* t, uint64_t cnt) {
+          tgb::bump_edges(g->g, up.p, t, cnt, per.p, tot.p, s);
+          T += cnt;
+        });
+        kp += tgb::sum_choose2(per.p, m, s);
+      }
+      k = tgb::sum_choose2(tot.p, m, s);
+    }
+    out3[0] = T;
+    out3[1] = k;
+    out3[2] = kp;
+    const double q3 = q * q * q;  // sparsify.hpp:148-152
+    var2[0] = (1.0 / q3 - 1.0) * (double)T + 2.0 * (double)k * (1.0 / q - 1.0);
+    var2[1] = (1.0 / q3 - 1.0) * (double)T + 2.0 * (double)kp * (1.0 / q - 1.0);
+  });
 }
 
 tg_status tg_clustering_coefficients(tg_graph* g, const tg_config* cfg, uint64_t* triangles_per_node,

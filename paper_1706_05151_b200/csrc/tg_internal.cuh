@@ -202,6 +202,23 @@ void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
 void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,
                        cudaStream_t s);
 
+// ---- analytics.cu (sequential.hpp:108-122, sparsify.hpp:113-155) ----
+// d_up (n+1): exclusive prefix of #neighbours above v (edges() order).
+void upper_offsets(const DevGraph& g, uint64_t* d_up, cudaStream_t s);
+// bump t_e of the three edges of each listed triple (ascending ids) into
+// d_te (and d_te2 when non-null).
+void bump_edges(const DevGraph& g, const uint64_t* d_up, const uint32_t* d_tri, uint64_t cnt,
+                unsigned long long* d_te, unsigned long long* d_te2, cudaStream_t s);
+// sum_e t_e (t_e - 1) / 2 (host result).
+uint64_t sum_choose2(const unsigned long long* d_te, uint64_t m, cudaStream_t s);
+
+// ---- sparsify.cu (sparsify.hpp) ----
+// Compact copy of `in` keeping entry u of row v iff keep_entry(q, seed, key,
+// v, u); key = kc, or owner(v)+1 under the plan d_b (p+1 entries, device)
+// when d_b != nullptr.  One host sync (entry count).
+void sparsify_eff(const DevEff& in, DevEff& out, double q, uint64_t seed, uint64_t kc,
+                  const uint32_t* d_b, uint64_t p, cudaStream_t s);
+
 // launch counter (kernels of ours launched), for bench's gpu_launches claim
 extern unsigned long long g_launches;
 // CTA-path shared-memory capacity in entries (0 = default); tests lower it

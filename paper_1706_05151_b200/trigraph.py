@@ -128,6 +128,12 @@ class Graph:
         off, adj = self.csr()
         return adj[off[v]:off[v + 1]]
 
+    def edges(self) -> np.ndarray:  # graph.hpp:40-46: (u, v), u < v, u then v ascending
+        off, adj = self.csr()
+        src = np.repeat(np.arange(len(off) - 1, dtype=np.uint32), np.diff(off).astype(np.int64))
+        keep = src < adj
+        return np.stack([src[keep], adj[keep]], axis=1)
+
 
 def build_graph(edge_pairs, n_override: int = 0, device: int = 0) -> Graph:
     """graph.hpp:58-85 -- drops self-loops, symmetrises, sorts and uniques on
@@ -256,6 +262,22 @@ def compute_boundaries(g: Graph, kind: CostKind, p: int) -> PartitionPlan:
     return PartitionPlan(b)
 
 
+class SparsifyMode(enum.IntEnum):  # sparsify.hpp:22-24 SparsifyConfig::Mode
+    PerPartition = 2
+    Global = 1
+
+
+@dataclass
+class SparsifyConfig:  # sparsify.hpp:22-33
+    q: float = 1.0
+    seed: int = 0
+    mode: SparsifyMode = SparsifyMode.Global
+
+    def validate(self):
+        if not (0.0 < self.q <= 1.0):
+            raise ValueError("sparsify: q must be in (0, 1]")
+
+
 @dataclass
 class EngineConfig:  # engines.hpp:270-280
     engine: EngineKind = EngineKind.Aop
@@ -265,6 +287,7 @@ class EngineConfig:  # engines.hpp:270-280
     mode: ExecMode = ExecMode.Interleaved
     track_nodes: bool = False
     collect_triangles: bool = False
+    sparsify: Optional[SparsifyConfig] = None
     boundaries: Optional[Sequence[int]] = None
 
 
@@ -305,6 +328,11 @@ def _cfg(cfg: EngineConfig):
         c.boundaries = keep.ctypes.data
     c.track_nodes = int(bool(cfg.track_nodes))
     c.collect_triangles = int(bool(cfg.collect_triangles))
+    if cfg.sparsify is not None:
+        cfg.sparsify.validate()  # engines.hpp:336
+        c.sparsify = int(cfg.sparsify.mode)
+        c.sparsify_q = float(cfg.sparsify.q)
+        c.sparsify_seed = int(cfg.sparsify.seed)
     return c, keep
 
 
@@ -356,6 +384,49 @@ def clustering_coefficients(g: Graph, cfg: EngineConfig) -> ClusteringResult:
     check(lib().tg_clustering_coefficients(g._h, C.byref(c), _p(tv), _p(cc)))
     del keep
     return ClusteringResult(tv[:n], cc[:n])
+
+
+def approx_count(g: Graph, p: int, engine: EngineKind, q: float, seed: int,
+                 mode: ExecMode = ExecMode.Interleaved, boundaries=None,
+                 cost: CostKind = CostKind.Dpd) -> float:
+    """engines.hpp:440-457: sparsify-then-count estimate T' / q^3 (AOP draws
+    per partition, the other engines one draw per edge)."""
+    keep = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=np.uint32)
+    out = C.c_double()
+    check(lib().tg_approx_count(g._h, int(p), int(engine), float(q), int(seed), _p(keep),
+                                int(cost), C.byref(out)))
+    return out.value
+
+
+def per_edge_triangle_counts(g: Graph) -> np.ndarray:
+    """sequential.hpp:108-122: t_e for every edge, in Graph::edges() order
+    (u < v; graph.hpp:40-46).  The reference returns a map keyed by (u, v);
+    pair it with ``Graph.edges()``."""
+    m = g.num_edges()
+    te = np.zeros(max(m, 1), dtype=np.uint64)
+    check(lib().tg_per_edge_triangle_counts(g._h, _p(te)))
+    return te[:m]
+
+
+@dataclass
+class VarianceReport:  # sparsify.hpp:113-121
+    triangles: int = 0
+    k: int = 0
+    k_prime: int = 0
+    q: float = 1.0
+    var: float = 0.0
+    var_prime: float = 0.0
+
+
+def variance_report(g: Graph, plan: PartitionPlan, q: float) -> VarianceReport:
+    """sparsify.hpp:113-155: k = pairs of triangles sharing an edge, k' =
+    those whose apexes have the same owner; variances of the 1/q^3 estimator."""
+    b = np.ascontiguousarray(plan.boundaries, dtype=np.uint32)
+    o3 = np.zeros(3, dtype=np.uint64)
+    v2 = np.zeros(2, dtype=np.float64)
+    check(lib().tg_variance_report(g._h, _p(b), b.shape[0] - 1, float(q), _p(o3), _p(v2)))
+    return VarianceReport(int(o3[0]), int(o3[1]), int(o3[2]), float(q), float(v2[0]),
+                          float(v2[1]))
 
 
 # ---------------------------------------------------------------- generators
