@@ -34,6 +34,27 @@ __device__ __forceinline__ bool contains_sub(const uint32_t* a, uint32_t n, uint
     if (pos + step <= n && a[pos + step - 1] < x) pos += step;
   return pos < n && a[pos] == x;
 }
+// the same search starting at step TOP (a power of two > n / 2): lists of a
+// group of short apexes need fewer than 6 steps
+template <uint32_t TOP>
+__device__ __forceinline__ bool contains_top(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t pos = 0;
+#pragma unroll
+  for (uint32_t step = TOP; step > 0; step >>= 1)
+    if (pos + step <= n && a[pos + step - 1] < x) pos += step;
+  return pos < n && a[pos] == x;
+}
+__device__ __forceinline__ bool contains_steps(const uint32_t* a, uint32_t n, uint32_t x,
+                                               uint32_t top) {
+  switch (top) {  // warp-uniform
+    case 1: return contains_top<1>(a, n, x);
+    case 2: return contains_top<2>(a, n, x);
+    case 4: return contains_top<4>(a, n, x);
+    case 8: return contains_top<8>(a, n, x);
+    case 16: return contains_top<16>(a, n, x);
+    default: return contains_top<32>(a, n, x);
+  }
+}
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 __global__ void __launch_bounds__(kGWarps * 32, 5)
@@ -52,6 +73,11 @@ k_intersect_group(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   __shared__ uint32_t sAv[kGWarps][32], sAex[kGWarps][32], sAh[kGWarps][32];  // apex slots
   __shared__ unsigned sCntV[kGWarps][32];  // per-apex found (tally)
   __shared__ const uint32_t* sAL[kGWarps][32];  // apex slot -> its list
+  // per-warp queue of one iteration's filter hits (<= 32 x kUnroll): the
+  // exact searches then run on full warps (Watts-Strogatz: ~1/3 of the
+  // elements close a triangle, so nearly every chunk has hits)
+  __shared__ uint32_t sQx[kGWarps][32 * kUnroll], sQa[kGWarps][32 * kUnroll];
+  __shared__ uint32_t sQj[(TALLY || LIST) ? kGWarps : 1][(TALLY || LIST) ? 32 * kUnroll : 1];
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
@@ -96,6 +122,9 @@ k_intersect_group(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       if (pos < big_cap) big[pos] = (uint32_t)k;
     }
     const uint32_t E = __shfl_sync(FULL, incl, take - 1);  // edges of the group
+    // search depth for the group's lists: largest power of two <= max h
+    const uint32_t gmax = __reduce_max_sync(FULL, in_group ? hh : 0u);
+    const uint32_t top = gmax ? 1u << (31 - __clz(gmax)) : 1u;
     const uint64_t gcur = cur;
     cur += take;
     if (E == 0) continue;
@@ -202,31 +231,43 @@ k_intersect_group(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             hits |= ((Bm[h >> 5] >> (h & 31)) & (unsigned)(xs[q] != kNoItem)) << q;
           }
           if (!__any_sync(FULL, hits != 0)) continue;
-          unsigned fnd = 0;
-#pragma unroll
-          for (int q = 0; q < kUnroll; ++q)
-            if ((hits >> q) & 1u)
-              fnd |= (unsigned)contains_sub(N + sAex[w][as[q]], sAh[w][as[q]], xs[q]) << q;
-          if (!__any_sync(FULL, fnd != 0)) continue;
+          // enqueue the hits, then search them 32 at a time
+          uint32_t nh = 0;
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            const uint32_t x = xs[q];
-            const bool found = (fnd >> q) & 1u;
+            const bool hit = (hits >> q) & 1u;
+            const unsigned m = __ballot_sync(FULL, hit);
+            const uint32_t pos = nh + __popc(m & lt_mask);
+            if (hit) {
+              sQx[w][pos] = xs[q];
+              sQa[w][pos] = as[q];
+              if (TALLY || LIST) sQj[w][pos] = jjs[q];
+            }
+            nh += __popc(m);
+          }
+          __syncwarp();
+          for (uint32_t i0 = 0; i0 < nh; i0 += 32) {
+            const bool in = i0 + lane < nh;
+            const uint32_t x = in ? sQx[w][i0 + lane] : kNoItem;
+            const uint32_t qa = in ? sQa[w][i0 + lane] : 0u;
+            const bool found = in && contains_steps(N + sAex[w][qa], sAh[w][qa], x, top);
             const unsigned m = __ballot_sync(FULL, found);
             grp_cnt += __popc(m);
             if (TALLY && found) {
               atomicAdd(&out.tally[x], 1ull);
-              atomicAdd(&sCntU[w][jjs[q]], 1u);
-              atomicAdd(&sCntV[w][as[q]], 1u);
+              atomicAdd(&sCntU[w][sQj[w][i0 + lane]], 1u);
+              atomicAdd(&sCntV[w][qa], 1u);
             }
             if (LIST && m) {
               unsigned long long b0 = 0;
               if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
               b0 = __shfl_sync(FULL, b0, 0);
               if (found)
-                emit_triple(out, b0 + __popc(m & lt_mask), sAv[w][as[q]], sU[w][jjs[q]], x);
+                emit_triple(out, b0 + __popc(m & lt_mask), sAv[w][qa], sU[w][sQj[w][i0 + lane]],
+                            x);
             }
           }
+          __syncwarp();
         }
         __syncwarp();
       }
