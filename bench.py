@@ -347,6 +347,44 @@ def run_ours(args):
     isect_avg = sum(isect_ms) / len(isect_ms)
     orient_avg = sum(a - b for a, b in zip(step_ms, isect_ms)) / len(step_ms)
 
+    # ---- e2e through the reference-facing C ABI with host buffers (every
+    # rank: upload its CSR copy, orient, count its AOP core, all-reduce)
+    off_h, adj_h = g.csr()
+    off_p = torch.from_numpy(off_h.view(np.int64)).pin_memory()
+    adj_p = torch.from_numpy(adj_h.view(np.int32)).pin_memory()
+    del off_h, adj_h
+    h2d = off_p.numel() * 8 + adj_p.numel() * 4
+    e2e_t = []
+    for i in range(args.e2e_warmup + args.e2e_steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = C.c_void_p()
+        check(L.tg_graph_from_csr(local, n, C.c_void_p(off_p.data_ptr()),
+                                  C.c_void_p(adj_p.data_ptr()), C.byref(h)))
+        if dist:
+            part = torch.zeros(1, dtype=torch.int64, device="cuda")
+            check(L.tg_set_stream(h, C.c_void_p(stream.cuda_stream)))
+            check(L.tg_aop_rank_device(h, bptr, ws, rank, C.c_void_p(part.data_ptr())))
+            dist.all_reduce(part)
+            cnt = int(part.item())  # 8-byte result back to the host
+        else:
+            c64 = C.c_uint64()
+            check(L.tg_count(h, C.byref(c64)))
+            cnt = c64.value
+        check(L.tg_graph_free(h))
+        t1 = time.perf_counter()
+        assert cnt == T_total
+        dt = t1 - t0
+        if dist:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        if i >= args.e2e_warmup:
+            e2e_t.append(dt)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+
     if rank != 0:
         return
     # ---- roofline of the intersection pass: 4 bytes x W algorithmic elements
@@ -361,28 +399,6 @@ def run_ours(args):
                 "kernel": "intersect pass (k_intersect_quad + k_intersect_ctaq)",
                 "algorithmic_bytes_per_pass": 4 * w_rank, "W": W,
                 "pass_ms": isect_avg, "orient_ms": orient_avg, "peak_source": peak_kind}
-
-    # ---- e2e through the reference-facing C ABI with host buffers
-    off_h, adj_h = g.csr()
-    off_p = torch.from_numpy(off_h.view(np.int64)).pin_memory()
-    adj_p = torch.from_numpy(adj_h.view(np.int32)).pin_memory()
-    del off_h, adj_h
-    h2d = off_p.numel() * 8 + adj_p.numel() * 4
-    e2e_t = []
-    for i in range(args.e2e_warmup + args.e2e_steps):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        h = C.c_void_p()
-        check(L.tg_graph_from_csr(local, n, C.c_void_p(off_p.data_ptr()),
-                                  C.c_void_p(adj_p.data_ptr()), C.byref(h)))
-        cnt = C.c_uint64()
-        check(L.tg_count(h, C.byref(cnt)))
-        check(L.tg_graph_free(h))
-        t1 = time.perf_counter()
-        assert cnt.value == T_total
-        if i >= args.e2e_warmup:
-            e2e_t.append(t1 - t0)
-    e2e_s = sum(e2e_t) / len(e2e_t)
 
     # ---- CPU baseline (reference on the host cores), bounded sample
     cpu = None
@@ -409,9 +425,12 @@ def run_ours(args):
         "elements_per_s": W / (ms_per_step / 1e3) / ws * ws,
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": 8, "ms_per_step": 1e3 * e2e_s,
-                "path": "tg_graph_from_csr(pinned host CSR) + tg_count + tg_graph_free"},
+        "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d * ws,
+                "d2h_bytes_per_step": 8 * ws, "ms_per_step": 1e3 * e2e_s,
+                "path": ("tg_graph_from_csr(pinned host CSR) + tg_count + tg_graph_free"
+                         if ws == 1 else
+                         "per rank: tg_graph_from_csr(pinned host CSR) + tg_aop_rank_device "
+                         "+ NCCL all-reduce + tg_graph_free; max over ranks")},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
