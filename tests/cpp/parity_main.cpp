@@ -78,6 +78,24 @@ int main(int argc, char** argv) {
     }
     CHECK(threw);
   }
+  {  // 8(f) rows: per-edge counts, q = 1 sparsification, variance report
+    // (sequential.hpp:108-122, engines.hpp:440-457, sparsify.hpp:113-155)
+    auto te = per_edge_triangle_counts(g5());
+    CHECK(te.size() == 6 && te.at({1, 2}) == 2 && te.at({0, 1}) == 1 && te.at({3, 4}) == 0);
+    std::vector<std::pair<NodeId, NodeId>> k8;
+    for (NodeId u = 0; u < 8; ++u)
+      for (NodeId v = u + 1; v < 8; ++v) k8.push_back({u, v});
+    auto gk = build_graph(k8, 8);
+    CHECK(approx_count(gk, 3, EngineKind::Aop, 1.0, 7) == 56.0);
+    EngineConfig sc = config(EngineKind::AnopSurrogate, 3);
+    sc.sparsify = SparsifyConfig{0.5, 11, SparsifyConfig::Mode::Global};
+    auto rs = run_engine(gk, sc);
+    auto rq = run_engine(gk, config(EngineKind::Sequential, 1));
+    CHECK(rs.total <= rq.total);
+    PartitionPlan plan{{0, 2, 5}};
+    auto vr = variance_report(g5(), plan, 0.5);
+    CHECK(vr.triangles == 2 && vr.k == 1 && vr.k_prime == 1 && vr.var == 16.0);
+  }
   {  // a PA graph through every engine: totals and per-rank sums agree
     auto g = gen_pa(20000, 20, 3);
     std::uint64_t t = count_node_iterator_n(g);
