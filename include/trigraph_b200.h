@@ -38,7 +38,8 @@ typedef enum {
   TG_ERR_CUDA = 2,
   TG_ERR_OOM = 3,
   TG_ERR_CAPACITY = 4, /* caller buffer too small; required size reported */
-  TG_ERR_INTERNAL = 5
+  TG_ERR_INTERNAL = 5,
+  TG_ERR_PARSE = 6 /* reference: trigraph::ParseError (io.hpp:18-22) */
 } tg_status;
 
 /* engines.hpp:24 EngineKind (same order). */
@@ -60,9 +61,19 @@ typedef enum {
   TG_COST_NOV = 6
 } tg_cost;
 
-/* engines.hpp:270-280 EngineConfig.  The order is always ByDegree (the
- * north_star path); ExecMode has no meaning on the device (results are
- * mode-independent, acceptance.cpp:438-468). */
+/* order.hpp:19 OrderKind::Tag (same order). */
+typedef enum {
+  TG_ORDER_BY_ID = 0,
+  TG_ORDER_BY_DEGREE = 1, /* the reference default and the hot path */
+  TG_ORDER_BY_RANDOM = 2, /* seeded Fisher-Yates, mt19937_64 */
+  TG_ORDER_BY_CORENESS = 3
+} tg_order;
+
+/* engines.hpp:270-280 EngineConfig.  ExecMode has no meaning on the device
+ * (results are mode-independent, acceptance.cpp:438-468).  A zero-
+ * initialised config keeps the graph's current order (ByDegree unless
+ * tg_set_order changed it); order_set = 1 selects OrderKind{order,
+ * order_seed} (EngineConfig::order, engines.hpp:274). */
 typedef struct {
   int32_t engine;            /* tg_engine */
   int32_t cost;              /* tg_cost, default TG_COST_DPD */
@@ -75,6 +86,9 @@ typedef struct {
   int32_t sparsify;
   double sparsify_q;
   uint64_t sparsify_seed;
+  int32_t order_set;         /* 0: the graph's current order */
+  int32_t order;             /* tg_order (when order_set) */
+  uint64_t order_seed;       /* ByRandom seed (OrderKind::seed) */
 } tg_config;
 
 /* sparsify.hpp:22-24 SparsifyConfig::Mode (0 = no sparsification). */
@@ -105,6 +119,13 @@ tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pa
 tg_status tg_graph_from_csr(int device, uint64_t n, const uint64_t* offsets,
                             const uint32_t* adj, tg_graph** out);
 tg_status tg_graph_free(tg_graph* g);
+/* build_graph(parse_edge_list(text), n_override) with both steps on the
+ * device (the CLI's --input path, cli.hpp:81-88).  text: len bytes, host or
+ * device.  On malformed input: TG_ERR_PARSE, *err_line (may be NULL) = the
+ * 1-based line of the first bad line, tg_last_error() = "line N: ..." (the
+ * ParseError message, io.hpp:18-22, 41-45). */
+tg_status tg_graph_from_text(int device, const char* text, uint64_t len, uint64_t n_override,
+                             tg_graph** out, uint64_t* err_line);
 /* Graph::num_nodes / num_edges (graph.hpp:25-26). */
 tg_status tg_graph_info(tg_graph* g, uint64_t* num_nodes, uint64_t* num_edges);
 /* Copy the CSR back (offsets n+1, adj 2m). */
@@ -114,12 +135,21 @@ tg_status tg_set_stream(tg_graph* g, void* stream);
 
 /* ---- preprocessing (order.hpp:95-104, effective.hpp:37-52) ---- */
 
-/* compute_order(g, ByDegree).rank (n entries). */
+/* Select the total order every later preprocessing and counting call on g
+ * orients by: compute_order(g, OrderKind{kind, seed}) (order.hpp:85-128).
+ * ByDegree (the default) keys on the degrees; ById, ByRandom(seed) and
+ * ByCoreness build their rank array on the device (ByRandom's sequential
+ * Fisher-Yates on the host).  Drops the cached oriented CSR when the order
+ * changes.  TG_ERR_INVALID_ARGUMENT for an unknown kind. */
+tg_status tg_set_order(tg_graph* g, int32_t kind, uint64_t seed);
+/* coreness(g) (order.hpp:39-83): core numbers, n entries (host). */
+tg_status tg_coreness(tg_graph* g, uint64_t* core);
+/* compute_order(g, <current order>).rank (n entries). */
 tg_status tg_compute_order(tg_graph* g, uint32_t* rank);
-/* effective_adjacency(g, degree order): offsets (n+1) and lists (m), either
- * may be NULL.  Builds and caches the oriented CSR on the device. */
+/* effective_adjacency(g, <current order>): offsets (n+1) and lists (m),
+ * either may be NULL.  Builds and caches the oriented CSR on the device. */
 tg_status tg_effective_adjacency(tg_graph* g, uint64_t* offsets, uint32_t* eff);
-/* ordering_cost(g, degree order) (sequential.hpp:95-104) = W. */
+/* ordering_cost(g, <current order>) (sequential.hpp:95-104) = W. */
 tg_status tg_ordering_cost(tg_graph* g, uint64_t* cost);
 
 /* ---- partitioning (partition.hpp:45-141) ---- */
@@ -131,14 +161,24 @@ tg_status tg_compute_boundaries(tg_graph* g, int32_t kind, uint64_t p, uint32_t*
 
 /* ---- counting (sequential.hpp:74-91, engines.hpp:335-435) ---- */
 
-/* count_node_iterator_n(effective_adjacency(g, by_degree)). */
+/* count_node_iterator_n(effective_adjacency(g, <current order>)). */
 tg_status tg_count(tg_graph* g, uint64_t* total);
+
+/* count_node_iterator_pp(g, <current order>, use_intersection)
+ * (sequential.hpp:48-70): the paper's NodeIterator++ baseline on the
+ * symmetric adjacency -- for every v < u < w in the order with u, w in
+ * adj(v), test (u, w).  Same count as tg_count; both reference variants
+ * (binary-search membership / merge intersection) compute the same sum, and
+ * the device runs membership searches for either. */
+tg_status tg_count_node_iterator_pp(tg_graph* g, int32_t use_intersection, uint64_t* total);
 
 /* run_engine(g, cfg).  per_rank: ranks entries (1 for SEQ); boundaries_out:
  * ranks+1 entries (may be NULL); node_counts: n entries, filled when
  * cfg->track_nodes; triangles: 3*capacity uint32, filled (ascending ids per
  * triple, unspecified triple order) when cfg->collect_triangles, with
- * *num_triangles = total; TG_ERR_CAPACITY if capacity < total. */
+ * *num_triangles = total; TG_ERR_CAPACITY if capacity < total.  A device
+ * `triangles` buffer with capacity >= total is written in place by the
+ * listing kernels (no staging copy). */
 tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total,
                         tg_rank_stats* per_rank, uint32_t* boundaries_out,
                         uint64_t* node_counts, uint32_t* triangles, uint64_t capacity,
@@ -152,18 +192,32 @@ tg_status tg_clustering_coefficients(tg_graph* g, const tg_config* cfg,
 
 /* approx_count(g, p, engine, q, seed, boundaries, cost) (engines.hpp:440-457):
  * sparsify-then-count estimate T' / q^3, PerPartition draws for AOP and
- * Global draws otherwise.  boundaries: optional (p+1 entries, host). */
+ * Global draws otherwise, under the degree order (the EngineConfig it builds
+ * keeps the default order).  boundaries: optional (p+1 entries, host). */
 tg_status tg_approx_count(tg_graph* g, uint64_t p, int32_t engine, double q, uint64_t seed,
                           const uint32_t* boundaries, int32_t cost, double* estimate);
 /* per_edge_triangle_counts(g, eff) (sequential.hpp:108-122): t_e for every
  * edge in Graph::edges() order (u < v, u then v ascending; graph.hpp:40-46);
  * te has num_edges entries (host or device memory). */
 tg_status tg_per_edge_triangle_counts(tg_graph* g, uint64_t* te);
-/* variance_report(g, plan, q) (sparsify.hpp:113-155): out3 = {T, k, k'},
+/* variance_report(g, plan, q) (sparsify.hpp:113-155; degree order, :123-124): out3 = {T, k, k'},
  * var2 = {var, var'} for the 1/q^3-scaled estimator under the plan given by
  * `boundaries` (p+1 entries, host). */
 tg_status tg_variance_report(tg_graph* g, const uint32_t* boundaries, uint64_t p, double q,
                              uint64_t* out3, double* var2);
+
+/* ---- edge-list text (io.hpp:24-64) ---- */
+
+/* parse_edge_list(text) on `device`: pairs (2*capacity uint32, host or
+ * device) get the (u, v) edges in file order, *num_pairs their count;
+ * TG_ERR_CAPACITY if capacity is smaller (count reported); pairs = NULL
+ * queries the count.  Errors as tg_graph_from_text. */
+tg_status tg_parse_edge_list(int device, const char* text, uint64_t len, uint32_t* pairs,
+                             uint64_t capacity, uint64_t* num_pairs, uint64_t* err_line);
+/* write_edge_list(g): "u v\n" per edge with u < v (io.hpp:52-64) into out
+ * (capacity bytes, host or device); *len = the full length;
+ * TG_ERR_CAPACITY if capacity < *len.  out may be NULL to query the size. */
+tg_status tg_write_edge_list(tg_graph* g, char* out, uint64_t capacity, uint64_t* len);
 
 /* ---- device-resident hot path (bench / multi-process drivers) ---- */
 

@@ -7,8 +7,8 @@
 //   namespace trigraph = trigraph_b200;     // same names, same semantics
 //
 // Names and argument meaning follow the reference (file:line cited per
-// symbol).  Differences: Graph lives on a CUDA device; the
-// order is always ByDegree; ExecMode is accepted and ignored;
+// symbol).  Differences: Graph lives on a CUDA device;
+// ExecMode is accepted and ignored;
 // RankStats::realized_cost is algorithmic work, not merge comparisons;
 // effective adjacency / order helpers take the Graph (the device keeps the
 // oriented CSR cached) instead of an EffectiveAdjacency / OrderRank.
@@ -22,6 +22,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -31,10 +32,18 @@ namespace trigraph_b200 {
 
 using NodeId = std::uint32_t;  // graph.hpp:14
 
+/// io.hpp:18-22.
+struct ParseError : std::runtime_error {
+  std::size_t line;
+  ParseError(std::size_t line_, const std::string& what_)
+      : std::runtime_error(what_), line(line_) {}
+};
+
 namespace detail {
-inline void check(tg_status s) {
+inline void check(tg_status s, std::uint64_t err_line = 0) {
   if (s == TG_OK) return;
   std::string msg = tg_last_error();
+  if (s == TG_ERR_PARSE) throw ParseError(err_line, msg);  // what() = "line N: ..."
   if (s == TG_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
   throw std::runtime_error(std::string(tg_status_string(s)) + ": " + msg);
 }
@@ -107,19 +116,48 @@ inline Graph build_graph(const std::vector<std::pair<NodeId, NodeId>>& edge_pair
   return Graph(h);
 }
 
-/// order.hpp:31-35 / :95-104 (ByDegree).
+/// order.hpp:17-28.
+struct OrderKind {
+  enum class Tag { ById, ByDegree, ByRandom, ByCoreness };
+  Tag tag = Tag::ByDegree;
+  std::uint64_t seed = 0;
+
+  static OrderKind by_id() { return {Tag::ById, 0}; }
+  static OrderKind by_degree() { return {Tag::ByDegree, 0}; }
+  static OrderKind by_random(std::uint64_t seed) { return {Tag::ByRandom, seed}; }
+  static OrderKind by_coreness() { return {Tag::ByCoreness, 0}; }
+};
+
+namespace detail {
+// The graph orients by `kind` from here on (tg_set_order).
+inline void use_order(const Graph& g, const OrderKind& kind) {
+  check(tg_set_order(g.handle(), static_cast<int32_t>(kind.tag), kind.seed));
+}
+}  // namespace detail
+
+/// order.hpp:31-35.
 struct OrderRank {
   std::vector<NodeId> rank;
   bool precedes(NodeId u, NodeId v) const { return rank[u] < rank[v]; }
 };
-inline OrderRank compute_order(const Graph& g) {
+/// order.hpp:85-128 for every OrderKind (ByRandom bit-identical to the
+/// reference's mt19937_64 Fisher-Yates).
+inline OrderRank compute_order(const Graph& g, OrderKind kind = OrderKind::by_degree()) {
+  detail::use_order(g, kind);
   OrderRank o;
   o.rank.resize(g.num_nodes());
   detail::check(tg_compute_order(g.handle(), o.rank.data()));
   return o;
 }
 
-/// effective.hpp:17-52 under the degree order.
+/// order.hpp:39-83 core numbers.
+inline std::vector<std::size_t> coreness(const Graph& g) {
+  std::vector<std::uint64_t> c(g.num_nodes());
+  detail::check(tg_coreness(g.handle(), c.data()));
+  return std::vector<std::size_t>(c.begin(), c.end());
+}
+
+/// effective.hpp:17-52 under `order` (default ByDegree).
 struct EffectiveAdjacency {
   std::vector<std::uint64_t> offsets{0};
   std::vector<NodeId> entries;
@@ -127,7 +165,9 @@ struct EffectiveAdjacency {
   std::size_t total_entries() const { return entries.size(); }
   std::size_t effdeg(NodeId v) const { return offsets[v + 1] - offsets[v]; }
 };
-inline EffectiveAdjacency effective_adjacency(const Graph& g) {
+inline EffectiveAdjacency effective_adjacency(const Graph& g,
+                                              OrderKind order = OrderKind::by_degree()) {
+  detail::use_order(g, order);
   EffectiveAdjacency e;
   e.offsets.resize(g.num_nodes() + 1);
   e.entries.resize(g.num_edges());
@@ -136,14 +176,27 @@ inline EffectiveAdjacency effective_adjacency(const Graph& g) {
 }
 
 /// sequential.hpp:74-91 (count only).
-inline std::uint64_t count_node_iterator_n(const Graph& g) {
+inline std::uint64_t count_node_iterator_n(const Graph& g,
+                                           OrderKind order = OrderKind::by_degree()) {
+  detail::use_order(g, order);
   std::uint64_t t = 0;
   detail::check(tg_count(g.handle(), &t));
   return t;
 }
 
-/// sequential.hpp:95-104 under the degree order.
-inline std::uint64_t ordering_cost(const Graph& g) {
+/// sequential.hpp:48-70 NodeIterator++ under `order` (the reference passes
+/// the OrderRank itself).
+inline std::uint64_t count_node_iterator_pp(const Graph& g, OrderKind order = OrderKind::by_degree(),
+                                            bool use_intersection = false) {
+  detail::use_order(g, order);
+  std::uint64_t t = 0;
+  detail::check(tg_count_node_iterator_pp(g.handle(), use_intersection ? 1 : 0, &t));
+  return t;
+}
+
+/// sequential.hpp:95-104 under `order` (default ByDegree).
+inline std::uint64_t ordering_cost(const Graph& g, OrderKind order = OrderKind::by_degree()) {
+  detail::use_order(g, order);
   std::uint64_t c = 0;
   detail::check(tg_ordering_cost(g.handle(), &c));
   return c;
@@ -154,7 +207,9 @@ struct CostVector {
   std::vector<std::uint64_t> f, prefix;
   std::uint64_t total() const { return prefix.empty() ? 0 : prefix.back(); }
 };
-inline CostVector node_costs(const Graph& g, CostKind kind) {
+inline CostVector node_costs(const Graph& g, CostKind kind,
+                             OrderKind order = OrderKind::by_degree()) {
+  detail::use_order(g, order);
   CostVector c;
   c.f.resize(g.num_nodes());
   c.prefix.resize(g.num_nodes());
@@ -179,8 +234,10 @@ struct PartitionPlan {
     return lo - 1;
   }
 };
-inline PartitionPlan compute_boundaries(const Graph& g, CostKind kind, std::size_t p) {
+inline PartitionPlan compute_boundaries(const Graph& g, CostKind kind, std::size_t p,
+                                        OrderKind order = OrderKind::by_degree()) {
   if (p == 0) throw std::invalid_argument("compute_boundaries: p must be >= 1");
+  detail::use_order(g, order);
   PartitionPlan plan;
   plan.boundaries.resize(p + 1);
   detail::check(tg_compute_boundaries(g.handle(), static_cast<int32_t>(kind), p,
@@ -204,6 +261,7 @@ struct EngineConfig {
   EngineKind engine = EngineKind::Aop;
   std::size_t ranks = 1;
   CostKind cost = CostKind::Dpd;
+  OrderKind order = OrderKind::by_degree();
   runtime::ExecMode mode = runtime::ExecMode::Interleaved;
   bool track_nodes = false;
   bool collect_triangles = false;
@@ -236,6 +294,9 @@ inline tg_config to_c(const EngineConfig& cfg) {
   c.boundaries = cfg.boundaries ? cfg.boundaries->data() : nullptr;
   c.track_nodes = cfg.track_nodes;
   c.collect_triangles = cfg.collect_triangles;
+  c.order_set = 1;  // engines.hpp:274
+  c.order = static_cast<int32_t>(cfg.order.tag);
+  c.order_seed = cfg.order.seed;
   if (cfg.sparsify) {
     cfg.sparsify->validate();
     c.sparsify = cfg.sparsify->mode == SparsifyConfig::Mode::PerPartition
@@ -262,7 +323,7 @@ inline RunReport run_engine(const Graph& g, const EngineConfig& cfg) {
   std::vector<tg_rank_stats> st(p);
   rep.boundaries.resize(p + 1);
   if (cfg.track_nodes) rep.node_counts.resize(g.num_nodes());
-  std::uint64_t cap = cfg.collect_triangles ? count_node_iterator_n(g) : 0, got = 0;
+  std::uint64_t cap = cfg.collect_triangles ? count_node_iterator_n(g, cfg.order) : 0, got = 0;
   std::vector<NodeId> flat(3 * cap);
   detail::check(tg_run_engine(g.handle(), &c, &rep.total, st.data(), rep.boundaries.data(),
                               cfg.track_nodes ? rep.node_counts.data() : nullptr,
@@ -334,6 +395,40 @@ inline VarianceReport variance_report(const Graph& g, const PartitionPlan& plan,
   double v2[2];
   detail::check(tg_variance_report(g.handle(), plan.boundaries.data(), plan.ranks(), q, o3, v2));
   return {o3[0], o3[1], o3[2], q, v2[0], v2[1]};
+}
+
+/// io.hpp:24-50 parse_edge_list, on the device.
+inline std::vector<std::pair<NodeId, NodeId>> parse_edge_list(std::string_view text,
+                                                              int device = 0) {
+  std::uint64_t cnt = 0, line = 0;
+  // (status first: the error line is only set once the call returned)
+  tg_status st = tg_parse_edge_list(device, text.data(), text.size(), nullptr, 0, &cnt, &line);
+  detail::check(st, line);
+  std::vector<std::uint32_t> flat(2 * cnt);
+  st = tg_parse_edge_list(device, text.data(), text.size(), flat.data(), cnt, &cnt, &line);
+  detail::check(st, line);
+  std::vector<std::pair<NodeId, NodeId>> out(cnt);
+  for (std::uint64_t k = 0; k < cnt; ++k) out[k] = {flat[2 * k], flat[2 * k + 1]};
+  return out;
+}
+
+/// build_graph(parse_edge_list(text), n_override) without the host round trip.
+inline Graph build_graph_from_text(std::string_view text, std::size_t n_override = 0,
+                                   int device = 0) {
+  tg_graph* h = nullptr;
+  std::uint64_t line = 0;
+  const tg_status st = tg_graph_from_text(device, text.data(), text.size(), n_override, &h, &line);
+  detail::check(st, line);
+  return Graph(h);
+}
+
+/// io.hpp:52-64 write_edge_list, on the device.
+inline std::string write_edge_list(const Graph& g) {
+  std::uint64_t len = 0;
+  detail::check(tg_write_edge_list(g.handle(), nullptr, 0, &len));
+  std::string out(len, '\0');
+  if (len) detail::check(tg_write_edge_list(g.handle(), &out[0], len, &len));
+  return out;
 }
 
 /// io.hpp:129-162 gen_pa (host, bit-identical edge stream).

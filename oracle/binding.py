@@ -22,6 +22,7 @@ P = C.c_void_p
 
 ENGINES = {"seq": 0, "aop": 1, "anop-direct": 2, "anop-surrogate": 3}
 COSTS = {"N": 0, "D": 1, "DH": 2, "DDH": 3, "DH2": 4, "DPD": 5, "NOV": 6}
+ORDERS = {"id": 0, "degree": 1, "random": 2, "coreness": 3}  # order.hpp:19 OrderKind::Tag
 
 _orc = None
 _ref = None
@@ -60,6 +61,12 @@ def lib():
             "orc_variance_report": (None, [u64, vp, vp, vp, u64, dbl, vp, vp]),
             "orc_cc": (None, [u64, vp, vp, vp]),
             "orc_random_graph_pairs": (u64, [u64, dbl, u64, vp, u64]),
+            "orc_coreness": (None, [u64, vp, vp, vp]),
+            "orc_parse_edge_list": (u64, [C.c_char_p, u64, vp, u64, vp, vp, vp, vp]),
+            "orc_write_edge_list": (u64, [u64, vp, vp, vp, u64]),
+            "orc_compute_order": (i32, [u64, vp, vp, i32, u64, vp]),
+            "orc_run_engine_ord": (u64, [u64, vp, vp, i32, u64, i32, vp, vp, vp, vp, vp,
+                                         vp, vp, vp, u64, i32, dbl, u64, i32, u64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -113,6 +120,13 @@ def ref():
             "ref_time_sequential": (dbl, [vp, vp]),
             "ref_prepare": (None, [vp]),
             "ref_aop_sample": (dbl, [vp, u64, vp, u64, i32, vp, vp]),
+            "ref_compute_order": (None, [vp, i32, u64, vp]),
+            "ref_coreness": (None, [vp, vp]),
+            "ref_parse_edge_list": (u64, [C.c_char_p, u64, vp, u64, vp, vp, u64]),
+            "ref_write_edge_list": (u64, [vp, vp, u64]),
+            "ref_effective_order": (u64, [vp, i32, u64, vp, vp, vp, vp]),
+            "ref_run_engine_order": (u64, [vp, i32, u64, i32, i32, u64, vp, vp, vp, vp, vp,
+                                           vp, u64, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -155,8 +169,24 @@ def degree_rank(g: CSR) -> np.ndarray:
     return r
 
 
-def effective(g: CSR):
-    rank = degree_rank(g)
+def compute_order(g: CSR, order="degree", seed: int = 0) -> np.ndarray:
+    """order.hpp:85-128 compute_order(g, OrderKind{order, seed}).rank."""
+    r = np.zeros(max(g.n, 1), dtype=U32)
+    if lib().orc_compute_order(g.n, _ptr(g.off), _ptr(g.adj), ORDERS[order], int(seed),
+                               _ptr(r)) != 0:
+        raise ValueError(f"unknown order {order!r}")
+    return r[: g.n]
+
+
+def coreness(g: CSR) -> np.ndarray:
+    """order.hpp:39-83 core numbers."""
+    c = np.zeros(max(g.n, 1), dtype=U64)
+    lib().orc_coreness(g.n, _ptr(g.off), _ptr(g.adj), _ptr(c))
+    return c[: g.n]
+
+
+def effective(g: CSR, order="degree", seed: int = 0):
+    rank = compute_order(g, order, seed)
     eoff = np.zeros(g.n + 1, dtype=U64)
     pe = C.c_void_p()
     m = lib().orc_effective(g.n, _ptr(g.off), _ptr(g.adj), _ptr(rank), _ptr(eoff), C.byref(pe))
@@ -165,8 +195,8 @@ def effective(g: CSR):
     return eoff, eff
 
 
-def count(g: CSR, tally=False, listing=False):
-    eoff, eff = effective(g)
+def count(g: CSR, tally=False, listing=False, order="degree", seed: int = 0):
+    eoff, eff = effective(g, order, seed)
     L = lib()
     T = L.orc_count(g.n, _ptr(eoff), _ptr(eff), None, None, 0)
     tv = np.zeros(g.n, dtype=U64) if tally else None
@@ -179,12 +209,13 @@ def count(g: CSR, tally=False, listing=False):
     return int(T), tv, tri
 
 
-def ordering_cost(g: CSR) -> int:
-    return int(lib().orc_ordering_cost(g.n, _ptr(g.off), _ptr(g.adj), _ptr(degree_rank(g))))
+def ordering_cost(g: CSR, order="degree", seed: int = 0) -> int:
+    return int(lib().orc_ordering_cost(g.n, _ptr(g.off), _ptr(g.adj),
+                                       _ptr(compute_order(g, order, seed))))
 
 
-def node_costs(g: CSR, kind: str):
-    eoff, eff = effective(g)
+def node_costs(g: CSR, kind: str, order="degree", seed: int = 0):
+    eoff, eff = effective(g, order, seed)
     f = np.zeros(g.n, dtype=U64)
     pre = np.zeros(g.n, dtype=U64)
     lib().orc_node_costs(g.n, _ptr(g.off), _ptr(g.adj), _ptr(eoff), _ptr(eff), COSTS[kind],
@@ -218,9 +249,10 @@ SPARSIFY = {None: 0, "global": 1, "per-partition": 2}
 
 def run_engine(g: CSR, engine="aop", ranks=1, cost="DPD", boundaries=None,
                track_nodes=False, collect_triangles=False, sparsify=None, q=1.0,
-               seed=0) -> Report:
+               seed=0, order="degree", order_seed=0) -> Report:
     """engines.hpp:335-418 run_engine via the C restatement; sparsify =
-    None | "global" | "per-partition" (SparsifyConfig, sparsify.hpp:22-33)."""
+    None | "global" | "per-partition" (SparsifyConfig, sparsify.hpp:22-33);
+    order = EngineConfig::order (engines.hpp:274)."""
     e = ENGINES[engine]
     p = 1 if engine == "seq" else int(ranks)
     if p == 0:
@@ -232,9 +264,10 @@ def run_engine(g: CSR, engine="aop", ranks=1, cost="DPD", boundaries=None,
     tv = np.zeros(g.n, dtype=U64) if track_nodes else None
     T, _, _ = count(g) if collect_triangles else (0, None, None)
     lst = np.zeros((max(T, 1), 3), dtype=U32) if collect_triangles else None
-    total = L.orc_run_engine_ex(g.n, _ptr(g.off), _ptr(g.adj), e, p, COSTS[cost], _ptr(bi),
-                                _ptr(bo), _ptr(tri), _ptr(sent), _ptr(recv), _ptr(st),
-                                _ptr(tv), _ptr(lst), T, SPARSIFY[sparsify], float(q), int(seed))
+    total = L.orc_run_engine_ord(g.n, _ptr(g.off), _ptr(g.adj), e, p, COSTS[cost], _ptr(bi),
+                                 _ptr(bo), _ptr(tri), _ptr(sent), _ptr(recv), _ptr(st),
+                                 _ptr(tv), _ptr(lst), T, SPARSIFY[sparsify], float(q), int(seed),
+                                 ORDERS[order], int(order_seed))
     if collect_triangles:
         T = min(T, int(total))  # sparsified runs list only the kept triangles
         lst = lst[:T]
@@ -270,6 +303,59 @@ def variance_report(g: CSR, boundaries, q):
     lib().orc_variance_report(g.n, _ptr(g.off), _ptr(g.adj), _ptr(b), len(b) - 1, float(q),
                               _ptr(o3), _ptr(v2))
     return int(o3[0]), int(o3[1]), int(o3[2]), float(v2[0]), float(v2[1])
+
+
+class ParseError(RuntimeError):
+    """io.hpp:18-22: ParseError(line, what) -> "line N: what"."""
+
+    def __init__(self, line: int, what: str):
+        super().__init__(f"line {line}: {what}")
+        self.line = line
+
+
+def parse_edge_list(text: bytes) -> np.ndarray:
+    """io.hpp:24-50 via the C restatement: (E, 2) uint32 pairs in file order."""
+    L = lib()
+    line = np.zeros(1, dtype=U64)
+    kind = np.zeros(1, dtype=np.int32)
+    tb = np.zeros(1, dtype=U64)
+    te = np.zeros(1, dtype=U64)
+    cnt = L.orc_parse_edge_list(text, len(text), None, 0, _ptr(line), _ptr(kind), _ptr(tb),
+                                _ptr(te))
+    if cnt == 2**64 - 1:
+        if int(kind[0]) == 1:
+            raise ParseError(int(line[0]), "expected two integer tokens")
+        tok = text[int(tb[0]):int(te[0])].decode("latin-1")
+        raise ParseError(int(line[0]), f"trailing token '{tok}'")
+    out = np.zeros((max(cnt, 1), 2), dtype=U32)
+    L.orc_parse_edge_list(text, len(text), _ptr(out), cnt, _ptr(line), _ptr(kind), _ptr(tb),
+                          _ptr(te))
+    return out[:cnt]
+
+
+def write_edge_list(g: CSR) -> bytes:
+    """io.hpp:52-64 via the C restatement."""
+    L = lib()
+    n = L.orc_write_edge_list(g.n, _ptr(g.off), _ptr(g.adj), None, 0)
+    buf = C.create_string_buffer(max(n, 1))
+    L.orc_write_edge_list(g.n, _ptr(g.off), _ptr(g.adj), C.cast(buf, vp_t), n)
+    return buf.raw[:n]
+
+
+vp_t = C.c_void_p
+
+
+def ref_parse_edge_list(text: bytes):
+    """The unmodified reference's parse_edge_list: pairs, or (line, message)."""
+    R = ref()
+    line = np.zeros(1, dtype=U64)
+    msg = C.create_string_buffer(512)
+    cnt = R.ref_parse_edge_list(text, len(text), None, 0, _ptr(line), C.cast(msg, vp_t), 512)
+    if cnt == 2**64 - 1:
+        return int(line[0]), msg.value.decode("latin-1")
+    out = np.zeros((max(cnt, 1), 2), dtype=U32)
+    R.ref_parse_edge_list(text, len(text), _ptr(out), cnt, _ptr(line), C.cast(msg, vp_t), 512)
+    return out[:cnt]
 
 
 def clustering(g: CSR, tv) -> np.ndarray:
@@ -332,6 +418,51 @@ class RefGraph:
         r = np.zeros(self.n, dtype=U32)
         ref().ref_degree_rank(self.h, _ptr(r))
         return r
+
+    def write_edge_list(self) -> bytes:
+        n = int(ref().ref_write_edge_list(self.h, None, 0))
+        buf = C.create_string_buffer(max(n, 1))
+        ref().ref_write_edge_list(self.h, C.cast(buf, vp_t), n)
+        return buf.raw[:n]
+
+    def compute_order(self, order="degree", seed=0):
+        r = np.zeros(max(self.n, 1), dtype=U32)
+        ref().ref_compute_order(self.h, ORDERS[order], int(seed), _ptr(r))
+        return r[: self.n]
+
+    def coreness(self):
+        c = np.zeros(max(self.n, 1), dtype=U64)
+        ref().ref_coreness(self.h, _ptr(c))
+        return c[: self.n]
+
+    def effective_order(self, order="degree", seed=0):
+        """(eoff, eff, count, ordering_cost) under compute_order(g, order)."""
+        o, sd = ORDERS[order], int(seed)
+        m = int(ref().ref_effective_order(self.h, o, sd, None, None, None, None))
+        eoff = np.zeros(self.n + 1, dtype=U64)
+        eff = np.zeros(max(m, 1), dtype=U32)
+        cnt = np.zeros(1, dtype=U64)
+        cost = np.zeros(1, dtype=U64)
+        ref().ref_effective_order(self.h, o, sd, _ptr(eoff), _ptr(eff), _ptr(cnt), _ptr(cost))
+        return eoff, eff[:m], int(cnt[0]), int(cost[0])
+
+    def run_engine_order(self, engine, ranks, order, order_seed=0, cost="DPD",
+                         track_nodes=False, collect_triangles=False):
+        e = ENGINES[engine]
+        p = 1 if engine == "seq" else int(ranks)
+        bo = np.zeros(max(p, 1) + 1, dtype=U32)
+        tri, sent, recv = (np.zeros(max(p, 1), dtype=U64) for _ in range(3))
+        tv = np.zeros(self.n, dtype=U64) if track_nodes else None
+        cap = self.count() if collect_triangles else 0
+        lst = np.zeros((max(cap, 1), 3), dtype=U32) if collect_triangles else None
+        nl = np.zeros(1, dtype=U64)
+        total = ref().ref_run_engine_order(self.h, e, int(ranks), COSTS[cost], ORDERS[order],
+                                           int(order_seed), _ptr(bo), _ptr(tri), _ptr(sent),
+                                           _ptr(recv), _ptr(tv), _ptr(lst), cap, _ptr(nl))
+        if total == 2**64 - 1:
+            raise ValueError("run_engine: ranks must be >= 1")
+        return Report(int(total), bo, tri, sent, recv, np.zeros(p, dtype=U64), tv,
+                      None if lst is None else lst[: int(nl[0])])
 
     def effective(self):
         m = int(ref().ref_effective(self.h, None, None))

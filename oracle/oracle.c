@@ -83,6 +83,115 @@ void orc_degree_rank(uint64_t n, const uint64_t* off, uint32_t* rank) {
   free(start);
 }
 
+/* order.hpp:39-83 coreness: the Batagelj-Zaversnik bucket peeling.  Nodes
+ * are processed in ascending current degree; core[v] = deg[v] at removal and
+ * every neighbour u with deg[u] > deg[v] moves down one bucket (:66-79). */
+void orc_coreness(uint64_t n, const uint64_t* off, const uint32_t* adj, uint64_t* core) {
+  uint64_t maxd = 0;
+  uint64_t* deg = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+  for (uint64_t v = 0; v < n; ++v) {
+    deg[v] = off[v + 1] - off[v];
+    if (deg[v] > maxd) maxd = deg[v];
+    core[v] = 0;
+  }
+  uint64_t* bin = (uint64_t*)calloc(maxd + 2, sizeof(uint64_t));
+  for (uint64_t v = 0; v < n; ++v) bin[deg[v] + 1]++;
+  for (uint64_t d = 0; d <= maxd; ++d) bin[d + 1] += bin[d];
+  uint32_t* order = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint64_t* pos = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+  uint64_t* start = (uint64_t*)malloc((maxd + 2) * sizeof(uint64_t));
+  memcpy(start, bin, (maxd + 2) * sizeof(uint64_t));
+  for (uint64_t v = 0; v < n; ++v) {
+    pos[v] = start[deg[v]]++;
+    order[pos[v]] = (uint32_t)v;
+  }
+  memcpy(start, bin, (maxd + 1) * sizeof(uint64_t));
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t v = order[i];
+    core[v] = deg[v];
+    for (uint64_t k = off[v]; k < off[v + 1]; ++k) {
+      const uint32_t u = adj[k];
+      if (deg[u] > deg[v]) {
+        const uint64_t du = deg[u], pu = pos[u], pw = start[du];
+        const uint32_t w = order[pw];
+        if (u != w) {
+          order[pu] = w;
+          order[pw] = u;
+          pos[u] = pw;
+          pos[w] = pu;
+        }
+        ++start[du];
+        --deg[u];
+      }
+    }
+  }
+  free(start);
+  free(pos);
+  free(order);
+  free(bin);
+  free(deg);
+}
+
+typedef struct {
+  uint64_t a, b, c;
+} key3_t;
+static const key3_t* g_sort_keys;
+static int cmp_key3_idx(const void* x, const void* y) {
+  const key3_t* p = &g_sort_keys[*(const uint32_t*)x];
+  const key3_t* q = &g_sort_keys[*(const uint32_t*)y];
+  if (p->a != q->a) return p->a < q->a ? -1 : 1;
+  if (p->b != q->b) return p->b < q->b ? -1 : 1;
+  return (p->c > q->c) - (p->c < q->c);
+}
+
+/* order.hpp:85-128 compute_order for every OrderKind::Tag (order.hpp:19):
+ * ById = identity (:90-93); ByDegree (:94-102); ByRandom = Fisher-Yates over
+ * mt19937_64(seed) with a modulo draw, i from n down to 2 (:104-113);
+ * ByCoreness = ascending (core, degree, id) (:114-124).  Returns -1 for an
+ * unknown kind. */
+int orc_compute_order(uint64_t n, const uint64_t* off, const uint32_t* adj, int kind,
+                      uint64_t seed, uint32_t* rank) {
+  if (kind == ORC_ORDER_BY_DEGREE) {
+    orc_degree_rank(n, off, rank);
+    return 0;
+  }
+  if (kind == ORC_ORDER_BY_ID) {
+    for (uint64_t v = 0; v < n; ++v) rank[v] = (uint32_t)v;
+    return 0;
+  }
+  uint32_t* nodes = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  for (uint64_t v = 0; v < n; ++v) nodes[v] = (uint32_t)v;
+  if (kind == ORC_ORDER_BY_RANDOM) {
+    orc_mt64 s;
+    orc_mt64_seed(&s, seed);
+    for (uint64_t i = n; i > 1; --i) {
+      const uint64_t j = orc_mt64_next(&s) % i;
+      const uint32_t x = nodes[i - 1];
+      nodes[i - 1] = nodes[j];
+      nodes[j] = x;
+    }
+  } else if (kind == ORC_ORDER_BY_CORENESS) {
+    uint64_t* core = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    orc_coreness(n, off, adj, core);
+    key3_t* keys = (key3_t*)malloc((n ? n : 1) * sizeof(key3_t));
+    for (uint64_t v = 0; v < n; ++v) {
+      keys[v].a = core[v];
+      keys[v].b = off[v + 1] - off[v];
+      keys[v].c = v;
+    }
+    g_sort_keys = keys;
+    qsort(nodes, n, sizeof(uint32_t), cmp_key3_idx);
+    free(keys);
+    free(core);
+  } else {
+    free(nodes);
+    return -1;
+  }
+  for (uint64_t i = 0; i < n; ++i) rank[nodes[i]] = (uint32_t)i;
+  free(nodes);
+  return 0;
+}
+
 /* effective.hpp:37-52: N_v = {u in adj(v) : rank[v] < rank[u]}, ID-sorted. */
 uint64_t orc_effective(uint64_t n, const uint64_t* off, const uint32_t* adj,
                        const uint32_t* rank, uint64_t* eoff, uint32_t** eff_out) {
@@ -435,11 +544,27 @@ uint64_t orc_run_engine_ex(uint64_t n, const uint64_t* off, const uint32_t* adj,
                            uint64_t* tri, uint64_t* sent, uint64_t* recv,
                            uint64_t* stored, uint64_t* tally, uint32_t* list,
                            uint64_t list_cap, int smode, double q, uint64_t seed) {
+  return orc_run_engine_ord(n, off, adj, engine, p, cost, boundaries_in, boundaries_out, tri,
+                            sent, recv, stored, tally, list, list_cap, smode, q, seed,
+                            ORC_ORDER_BY_DEGREE, 0);
+}
+
+/* engines.hpp:335-418 with cfg.order (:274, compute_order at :341). */
+uint64_t orc_run_engine_ord(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                            int engine, uint64_t p, int cost,
+                            const uint32_t* boundaries_in, uint32_t* boundaries_out,
+                            uint64_t* tri, uint64_t* sent, uint64_t* recv,
+                            uint64_t* stored, uint64_t* tally, uint32_t* list,
+                            uint64_t list_cap, int smode, double q, uint64_t seed,
+                            int order, uint64_t order_seed) {
   /* engines.hpp:337-338 */
   if (engine == ORC_ENGINE_SEQ) p = 1;
   if (p == 0) return UINT64_MAX;
   uint32_t* rank = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
-  orc_degree_rank(n, off, rank);
+  if (orc_compute_order(n, off, adj, order, order_seed, rank) != 0) {
+    free(rank);
+    return UINT64_MAX;
+  }
   uint64_t* eoff = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
   uint32_t* eff = NULL;
   orc_effective(n, off, adj, rank, eoff, &eff);
@@ -678,6 +803,112 @@ void orc_cc(uint64_t n, const uint64_t* off, const uint64_t* tally, double* c) {
     uint64_t d = off[v + 1] - off[v];
     c[v] = d >= 2 ? 2.0 * (double)tally[v] / ((double)d * (double)(d - 1)) : 0.0;
   }
+}
+
+/* ---- edge-list text (io.hpp:18-64) ------------------------------------ */
+
+/* std::isspace in the "C" locale (istream >> skips these). */
+static int orc_isspace(unsigned char c) {
+  return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+
+/* istream >> unsigned long long, as libstdc++'s num_get extracts it: skip
+ * whitespace, optional sign, one or more decimal digits; overflow fails;
+ * '-' negates modulo 2^64.  Returns 1 on success. */
+static int orc_extract_ull(const char* s, uint64_t n, uint64_t* i, uint64_t* out) {
+  while (*i < n && orc_isspace((unsigned char)s[*i])) ++*i;
+  if (*i >= n) return 0;
+  int neg = 0;
+  if (s[*i] == '+' || s[*i] == '-') {
+    neg = s[*i] == '-';
+    ++*i;
+  }
+  if (*i >= n || s[*i] < '0' || s[*i] > '9') return 0;
+  uint64_t acc = 0;
+  int over = 0;
+  while (*i < n && s[*i] >= '0' && s[*i] <= '9') {
+    const uint64_t d = (uint64_t)(s[*i] - '0');
+    if (acc > (UINT64_MAX - d) / 10) over = 1;
+    else acc = acc * 10 + d;
+    ++*i;
+  }
+  if (over) return 0;
+  *out = neg ? (uint64_t)0 - acc : acc;
+  return 1;
+}
+
+/* io.hpp:24-50 parse_edge_list.  Lines split at '\n' (:29-35); a line whose
+ * first byte outside " \t\r" is absent or '#' is skipped (:37-39); then two
+ * unsigned extractions (:41-43) and no further token (:44-45); ids are the
+ * values truncated to NodeId (:46).  Returns the pair count (pairs written
+ * up to cap), or UINT64_MAX on a ParseError with *err_line (1-based),
+ * *err_kind (1 = "expected two integer tokens", 2 = "trailing token") and,
+ * for kind 2, the token's byte range [*tok_b, *tok_e). */
+uint64_t orc_parse_edge_list(const char* text, uint64_t len, uint32_t* pairs, uint64_t cap,
+                             uint64_t* err_line, int* err_kind, uint64_t* tok_b,
+                             uint64_t* tok_e) {
+  uint64_t count = 0, lineno = 0, pos = 0;
+  while (pos < len) {
+    uint64_t end = pos;
+    while (end < len && text[end] != '\n') ++end;
+    const uint64_t b = pos, e = end;
+    pos = end + 1;
+    ++lineno;
+    uint64_t first = b;
+    while (first < e && (text[first] == ' ' || text[first] == '\t' || text[first] == '\r'))
+      ++first;
+    if (first == e || text[first] == '#') continue;
+    uint64_t i = b, u = 0, v = 0;
+    if (!orc_extract_ull(text, e, &i, &u) || !orc_extract_ull(text, e, &i, &v)) {
+      *err_line = lineno;
+      *err_kind = 1;
+      return UINT64_MAX;
+    }
+    while (i < e && orc_isspace((unsigned char)text[i])) ++i;
+    if (i < e) {
+      uint64_t j = i;
+      while (j < e && !orc_isspace((unsigned char)text[j])) ++j;
+      *err_line = lineno;
+      *err_kind = 2;
+      *tok_b = i;
+      *tok_e = j;
+      return UINT64_MAX;
+    }
+    if (count < cap) {
+      pairs[2 * count] = (uint32_t)u;
+      pairs[2 * count + 1] = (uint32_t)v;
+    }
+    ++count;
+  }
+  return count;
+}
+
+/* io.hpp:52-64 write_edge_list: "u v\n" for every edge with u < v, u then
+ * neighbour order.  Writes up to cap bytes; returns the full length. */
+uint64_t orc_write_edge_list(uint64_t n, const uint64_t* off, const uint32_t* adj, char* out,
+                             uint64_t cap) {
+  uint64_t w = 0;
+  char buf[32];
+  for (uint64_t u = 0; u < n; ++u)
+    for (uint64_t k = off[u]; k < off[u + 1]; ++k) {
+      if (u >= adj[k]) continue;
+      int len = 0;
+      uint64_t x = adj[k];
+      char tmp[12];
+      int t = 0;
+      do { tmp[t++] = (char)('0' + x % 10); x /= 10; } while (x);
+      uint64_t y = u;
+      char tu[12];
+      int tl = 0;
+      do { tu[tl++] = (char)('0' + y % 10); y /= 10; } while (y);
+      while (tl) buf[len++] = tu[--tl];
+      buf[len++] = ' ';
+      while (t) buf[len++] = tmp[--t];
+      buf[len++] = '\n';
+      for (int c = 0; c < len; ++c, ++w)
+        if (w < cap) out[w] = buf[c];
+    }
+  return w;
 }
 
 /* ---- fixtures -------------------------------------------------------- */

@@ -33,6 +33,17 @@ void orc_free(void* p);
  * (degree, id) ascending sort. */
 void orc_degree_rank(uint64_t n, const uint64_t* off, uint32_t* rank);
 
+/* order.hpp:19 OrderKind::Tag, in declaration order. */
+enum { ORC_ORDER_BY_ID = 0, ORC_ORDER_BY_DEGREE, ORC_ORDER_BY_RANDOM, ORC_ORDER_BY_CORENESS };
+
+/* order.hpp:39-83 coreness (core numbers, n entries). */
+void orc_coreness(uint64_t n, const uint64_t* off, const uint32_t* adj, uint64_t* core);
+
+/* order.hpp:85-128 compute_order(g, OrderKind{kind, seed}).rank.  Returns 0,
+ * or -1 for an unknown kind. */
+int orc_compute_order(uint64_t n, const uint64_t* off, const uint32_t* adj, int kind,
+                      uint64_t seed, uint32_t* rank);
+
 /* effective.hpp:37-52.  eoff has n+1 entries (caller-allocated);
  * *eff_out (m entries) malloc'ed.  Returns m. */
 uint64_t orc_effective(uint64_t n, const uint64_t* off, const uint32_t* adj,
@@ -48,7 +59,7 @@ uint64_t orc_count(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
 uint64_t orc_count_range(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
                          uint64_t vlo, uint64_t vhi);
 
-/* sequential.hpp:95-104 ordering_cost under the degree order. */
+/* sequential.hpp:95-104 ordering_cost under the order given by rank. */
 uint64_t orc_ordering_cost(uint64_t n, const uint64_t* off, const uint32_t* adj,
                            const uint32_t* rank);
 
@@ -94,6 +105,16 @@ uint64_t orc_run_engine_ex(uint64_t n, const uint64_t* off, const uint32_t* adj,
                            uint64_t* stored, uint64_t* tally, uint32_t* list,
                            uint64_t list_cap, int smode, double q, uint64_t seed);
 
+/* orc_run_engine_ex under EngineConfig::order = OrderKind{order, order_seed}
+ * (engines.hpp:274, :341).  UINT64_MAX also for an unknown order. */
+uint64_t orc_run_engine_ord(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                            int engine, uint64_t p, int cost,
+                            const uint32_t* boundaries_in, uint32_t* boundaries_out,
+                            uint64_t* tri, uint64_t* sent, uint64_t* recv,
+                            uint64_t* stored, uint64_t* tally, uint32_t* list,
+                            uint64_t list_cap, int smode, double q, uint64_t seed,
+                            int order, uint64_t order_seed);
+
 /* sparsify.hpp:58-62 keep_entry with a resolved rank key. */
 int orc_keep_entry(double q, uint64_t seed, uint64_t rank_key, uint32_t v, uint32_t u);
 
@@ -109,6 +130,18 @@ void orc_per_edge_counts(uint64_t n, const uint64_t* off, const uint32_t* adj, u
 void orc_variance_report(uint64_t n, const uint64_t* off, const uint32_t* adj,
                          const uint32_t* b, uint64_t p, double q, uint64_t* out3,
                          double* var2);
+
+/* io.hpp:24-50 parse_edge_list.  Returns the pair count (at most cap pairs
+ * written, interleaved), or UINT64_MAX on ParseError: *err_line (1-based),
+ * *err_kind 1 = "expected two integer tokens", 2 = "trailing token" (token
+ * bytes [*tok_b, *tok_e) of text). */
+uint64_t orc_parse_edge_list(const char* text, uint64_t len, uint32_t* pairs, uint64_t cap,
+                             uint64_t* err_line, int* err_kind, uint64_t* tok_b,
+                             uint64_t* tok_e);
+
+/* io.hpp:52-64 write_edge_list; writes up to cap bytes, returns the length. */
+uint64_t orc_write_edge_list(uint64_t n, const uint64_t* off, const uint32_t* adj, char* out,
+                             uint64_t cap);
 
 /* engines.hpp:422-435 clustering coefficient formula. */
 void orc_cc(uint64_t n, const uint64_t* off, const uint64_t* tally, double* c);

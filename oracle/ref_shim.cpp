@@ -12,6 +12,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -101,6 +102,48 @@ void ref_degree_rank(void* h, uint32_t* rank) {
   std::memcpy(rank, ord.rank.data(), ord.rank.size() * sizeof(uint32_t));
 }
 
+OrderKind order_kind(int kind, uint64_t seed) {
+  switch (kind) {
+    case 0: return OrderKind::by_id();
+    case 1: return OrderKind::by_degree();
+    case 2: return OrderKind::by_random(seed);
+    default: return OrderKind::by_coreness();
+  }
+}
+
+// compute_order(g, OrderKind{kind, seed}) (order.hpp:85-128).
+void ref_compute_order(void* h, int kind, uint64_t seed, uint32_t* rank) {
+  auto ord = compute_order(static_cast<RefGraph*>(h)->g, order_kind(kind, seed));
+  std::memcpy(rank, ord.rank.data(), ord.rank.size() * sizeof(uint32_t));
+}
+
+// coreness(g) (order.hpp:39-83).
+void ref_coreness(void* h, uint64_t* core) {
+  auto c = coreness(static_cast<RefGraph*>(h)->g);
+  for (std::size_t v = 0; v < c.size(); ++v) core[v] = c[v];
+}
+
+// effective_adjacency(g, compute_order(g, kind)) + count_node_iterator_n +
+// ordering_cost under that order.  eoff (n+1) / eff (m) may be NULL.
+uint64_t ref_effective_order(void* h, int kind, uint64_t seed, uint64_t* eoff, uint32_t* eff,
+                             uint64_t* count, uint64_t* cost) {
+  const Graph& g = static_cast<RefGraph*>(h)->g;
+  auto ord = compute_order(g, order_kind(kind, seed));
+  auto e = effective_adjacency(g, ord);
+  uint64_t k = 0;
+  if (eoff) eoff[0] = 0;
+  for (NodeId v = 0; v < e.num_nodes(); ++v) {
+    for (NodeId u : e.eff(v)) {
+      if (eff) eff[k] = u;
+      ++k;
+    }
+    if (eoff) eoff[v + 1] = k;
+  }
+  if (count) *count = count_node_iterator_n(e);
+  if (cost) *cost = ordering_cost(g, ord);
+  return k;
+}
+
 uint64_t ref_effective(void* h, uint64_t* eoff, uint32_t* eff) {
   const auto& e = static_cast<RefGraph*>(h)->effective();
   const uint64_t n = e.num_nodes();
@@ -171,6 +214,68 @@ uint64_t ref_run_engine(void* h, int engine, uint64_t p, int cost, const uint32_
   cfg.collect_triangles = list != nullptr;
   uint64_t pp = cfg.engine == EngineKind::Sequential ? 1 : p;
   if (b_in) cfg.boundaries = std::vector<NodeId>(b_in, b_in + pp + 1);
+  RunReport rep;
+  try {
+    rep = run_engine(r->g, cfg);
+  } catch (const std::invalid_argument&) {
+    return UINT64_MAX;
+  }
+  std::memcpy(b_out, rep.boundaries.data(), rep.boundaries.size() * sizeof(uint32_t));
+  for (std::size_t i = 0; i < rep.per_rank.size(); ++i) {
+    tri[i] = rep.per_rank[i].triangles;
+    sent[i] = rep.per_rank[i].data_sent;
+    recv[i] = rep.per_rank[i].data_recv;
+  }
+  if (tally)
+    std::memcpy(tally, rep.node_counts.data(), rep.node_counts.size() * sizeof(uint64_t));
+  if (list) {
+    std::sort(rep.triangles_list.begin(), rep.triangles_list.end());
+    *n_listed = rep.triangles_list.size();
+    for (uint64_t k = 0; k < rep.triangles_list.size() && k < cap; ++k)
+      for (int c = 0; c < 3; ++c) list[3 * k + c] = rep.triangles_list[k][c];
+  }
+  return rep.total;
+}
+
+// parse_edge_list (io.hpp:24-50).  Returns the pair count (up to cap pairs
+// written) or UINT64_MAX on ParseError, with *err_line and the message
+// (what()) copied into msg (msg_cap bytes, NUL-terminated).
+uint64_t ref_parse_edge_list(const char* text, uint64_t len, uint32_t* pairs, uint64_t cap,
+                             uint64_t* err_line, char* msg, uint64_t msg_cap) {
+  try {
+    auto e = parse_edge_list(std::string_view(text, len));
+    for (uint64_t k = 0; k < e.size() && k < cap; ++k) {
+      pairs[2 * k] = e[k].first;
+      pairs[2 * k + 1] = e[k].second;
+    }
+    return e.size();
+  } catch (const ParseError& err) {
+    *err_line = err.line;
+    std::snprintf(msg, msg_cap, "%s", err.what());
+    return UINT64_MAX;
+  }
+}
+
+// write_edge_list (io.hpp:52-64): up to cap bytes; returns the length.
+uint64_t ref_write_edge_list(void* h, char* out, uint64_t cap) {
+  auto s = write_edge_list(static_cast<RefGraph*>(h)->g);
+  std::memcpy(out, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
+}
+
+// run_engine with cfg.order = OrderKind{order, order_seed} (engines.hpp:274).
+uint64_t ref_run_engine_order(void* h, int engine, uint64_t p, int cost, int order,
+                              uint64_t order_seed, uint32_t* b_out, uint64_t* tri,
+                              uint64_t* sent, uint64_t* recv, uint64_t* tally, uint32_t* list,
+                              uint64_t cap, uint64_t* n_listed) {
+  auto* r = static_cast<RefGraph*>(h);
+  EngineConfig cfg;
+  cfg.engine = static_cast<EngineKind>(engine);
+  cfg.ranks = p;
+  cfg.cost = static_cast<CostKind>(cost);
+  cfg.order = order_kind(order, order_seed);
+  cfg.track_nodes = tally != nullptr;
+  cfg.collect_triangles = list != nullptr;
   RunReport rep;
   try {
     rep = run_engine(r->g, cfg);

@@ -19,6 +19,7 @@ TG_ERR_CUDA = 2
 TG_ERR_OOM = 3
 TG_ERR_CAPACITY = 4
 TG_ERR_INTERNAL = 5
+TG_ERR_PARSE = 6
 
 
 class TgConfig(C.Structure):
@@ -32,6 +33,9 @@ class TgConfig(C.Structure):
         ("sparsify", C.c_int32),
         ("sparsify_q", C.c_double),
         ("sparsify_seed", C.c_uint64),
+        ("order_set", C.c_int32),
+        ("order", C.c_int32),
+        ("order_seed", C.c_uint64),
     ]
 
 
@@ -55,12 +59,18 @@ SIGNATURES = {
     "tg_graph_info": (_i32, [_vp, _pu64, _pu64]),
     "tg_graph_csr": (_i32, [_vp, _vp, _vp]),
     "tg_set_stream": (_i32, [_vp, _vp]),
+    "tg_set_order": (_i32, [_vp, _i32, _u64]),
+    "tg_graph_from_text": (_i32, [C.c_int, _vp, _u64, _u64, _pvp, _pu64]),
+    "tg_parse_edge_list": (_i32, [C.c_int, _vp, _u64, _vp, _u64, _pu64, _pu64]),
+    "tg_write_edge_list": (_i32, [_vp, _vp, _u64, _pu64]),
+    "tg_coreness": (_i32, [_vp, _vp]),
     "tg_compute_order": (_i32, [_vp, _vp]),
     "tg_effective_adjacency": (_i32, [_vp, _vp, _vp]),
     "tg_ordering_cost": (_i32, [_vp, _pu64]),
     "tg_node_costs": (_i32, [_vp, _i32, _vp, _vp]),
     "tg_compute_boundaries": (_i32, [_vp, _i32, _u64, _vp]),
     "tg_count": (_i32, [_vp, _pu64]),
+    "tg_count_node_iterator_pp": (_i32, [_vp, _i32, _pu64]),
     "tg_run_engine": (_i32, [_vp, C.POINTER(TgConfig), _pu64, _vp, _vp, _vp, _vp, _u64, _pu64]),
     "tg_clustering_coefficients": (_i32, [_vp, C.POINTER(TgConfig), _vp, _vp]),
     "tg_approx_count": (_i32, [_vp, _u64, _i32, _dbl, _u64, _vp, _i32, C.POINTER(_dbl)]),
@@ -113,11 +123,21 @@ def lib():
     return _lib
 
 
-def check(status: int) -> None:
+class ParseError(RuntimeError):
+    """io.hpp:18-22 trigraph::ParseError: what() = "line N: ...", .line = N."""
+
+    def __init__(self, line: int, msg: str):
+        super().__init__(msg)
+        self.line = line
+
+
+def check(status: int, err_line: int = 0) -> None:
     """Map tg_status to the reference's exception types."""
     if status == TG_OK:
         return
     msg = lib().tg_last_error().decode(errors="replace")
+    if status == TG_ERR_PARSE:
+        raise ParseError(err_line, msg)
     if status == TG_ERR_INVALID_ARGUMENT:
         raise ValueError(msg)  # reference: std::invalid_argument
     if status == TG_ERR_OOM:

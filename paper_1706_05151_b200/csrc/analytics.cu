@@ -1,7 +1,8 @@
 // analytics.cu -- per-edge triangle counts and the sparsification variance
-// analytics.
+// analytics, and the NodeIterator++ baseline.
 //
 // Reference (paths relative to /root/reference/proj/include/trigraph/):
+//   count_node_iterator_pp     sequential.hpp:48-70
 //   per_edge_triangle_counts   sequential.hpp:108-122
 //   variance_report            sparsify.hpp:113-155
 //   Graph::edges() order       graph.hpp:40-46
@@ -27,6 +28,52 @@ __device__ __forceinline__ uint64_t lb_u32(const uint32_t* __restrict__ a, uint6
     else hi = mid;
   }
   return lo;
+}
+
+__device__ __forceinline__ bool has_in(const uint32_t* __restrict__ a, uint64_t b, uint64_t e,
+                                       uint32_t x) {
+  while (b < e) {
+    const uint64_t mid = (b + e) >> 1;
+    const uint32_t y = a[mid];
+    if (y == x) return true;
+    if (y < x) b = mid + 1;
+    else e = mid;
+  }
+  return false;
+}
+
+__device__ __forceinline__ bool key_precedes(uint32_t kv, uint32_t v, uint32_t ku, uint32_t u) {
+  return kv < ku || (kv == ku && v < u);
+}
+
+// NodeIterator++ (sequential.hpp:51-70) on the symmetric adjacency: a warp
+// per v walks its neighbours u with v < u in the order; lanes split adj(v)
+// and test each w with u < w for membership in adj(u) (Graph::has_edge, a
+// binary search, graph.hpp:34-38).  `key` is the order key (degree, or the
+// rank of a non-degree order).
+__global__ void __launch_bounds__(256)
+k_node_iterator_pp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                   const uint32_t* __restrict__ key, uint64_t n,
+                   unsigned long long* __restrict__ total) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t c = 0;
+  for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+    const uint32_t kv = key[v];
+    const uint64_t b = off[v], e = off[v + 1];
+    for (uint64_t j = b; j < e; ++j) {
+      const uint32_t u = adj[j];
+      const uint32_t ku = key[u];
+      if (!key_precedes(kv, (uint32_t)v, ku, u)) continue;
+      const uint64_t ub = off[u], ue = off[u + 1];
+      for (uint64_t k = b + lane; k < e; k += 32) {
+        const uint32_t w = adj[k];
+        if (key_precedes(ku, u, key[w], w) && has_in(adj, ub, ue, w)) ++c;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0 && c) atomicAdd(total, (unsigned long long)c);
 }
 
 // #neighbours above v (edges() emits (v, u) for u > v)
@@ -77,6 +124,21 @@ __global__ void k_choose2(const unsigned long long* __restrict__ te, uint64_t m,
 }
 
 }  // namespace
+
+uint64_t node_iterator_pp_device(const DevGraph& g, cudaStream_t s) {
+  DBuf<unsigned long long> acc(1, s);
+  acc.zero();
+  if (g.n) {
+    k_node_iterator_pp<<<grid_for(g.n * 32, 256, 148u * 32u), 256, 0, s>>>(g.off.p, g.adj.p,
+                                                                          order_key(g), g.n, acc.p);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
+  }
+  unsigned long long h = 0;
+  TG_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
 
 void upper_offsets(const DevGraph& g, uint64_t* d_up, cudaStream_t s) {
   TG_CUDA(cudaMemsetAsync(d_up, 0, 8, s));

@@ -44,7 +44,7 @@ struct tg_graph {
   // re-home stream-ordered frees when the caller switches streams)
   template <class F>
   void for_each_buf(F&& f) {
-    f(g.off); f(g.adj); f(g.deg); f(g.dcode);
+    f(g.off); f(g.adj); f(g.deg); f(g.dcode); f(g.okey);
     f(eff.off); f(eff.data); f(eff.desc);
     f(scr.big); f(scr.big_count);
     f(part.off); f(part.data); f(part.desc);
@@ -135,6 +135,17 @@ tg_graph* new_graph(int device) {
   return g;
 }
 
+// Orient by OrderKind{kind, seed} from now on (order.hpp:85-128); the cached
+// oriented CSR and rank partitions are dropped when the order changes.
+void apply_order(tg_graph* g, int kind, uint64_t seed) {
+  TG_REQUIRE(kind >= TG_ORDER_BY_ID && kind <= TG_ORDER_BY_CORENESS, "unknown order kind");
+  const uint64_t sd = kind == TG_ORDER_BY_RANDOM ? seed : 0;
+  if (g->g.order == kind && g->g.order_seed == sd) return;
+  tgb::set_order(g->g, kind, sd, g->stream);
+  g->have_eff = false;
+  g->have_part = false;
+}
+
 void ensure_eff(tg_graph* g) {
   if (!g->have_eff) {
     tgb::orient_full(g->g, g->eff, g->stream);
@@ -193,6 +204,7 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
   TG_REQUIRE(p >= 1, "run_engine: ranks must be >= 1");  // engines.hpp:337-338
   TG_REQUIRE(cfg.cost >= TG_COST_N && cfg.cost <= TG_COST_NOV, "unknown cost kind");
   cudaStream_t s = g->stream;
+  if (cfg.order_set) apply_order(g, cfg.order, cfg.order_seed);  // engines.hpp:341
   ensure_eff(g);
   const uint64_t n = g->g.n;
   EngineResult R;
@@ -416,6 +428,48 @@ constexpr uint64_t kListCap = 1ull << 26;  // triples per listing piece (768 MB)
 
 }  // namespace
 
+namespace {
+
+// The text in a device buffer padded with 16 zero bytes past len (the parse
+// kernels read aligned 16-byte groups); a host text is uploaded into it.
+void stage_text(const char* text, uint64_t len, DBuf<char>& buf, cudaStream_t s) {
+  buf.alloc(len + 32, s);
+  TG_CUDA(cudaMemsetAsync(buf.p + len, 0, 32, s));
+  if (len)
+    TG_CUDA(cudaMemcpyAsync(buf.p, text, len,
+                            is_device_ptr(text) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+}
+
+struct ParseFailure {
+  uint64_t line;
+  std::string msg;
+};
+
+// parse_edge_list on the device; throws ParseFailure (mapped to TG_ERR_PARSE)
+uint64_t parse_text(const char* text, uint64_t len, DBuf<uint32_t>& pairs, cudaStream_t s) {
+  DBuf<char> buf;
+  stage_text(text, len, buf, s);
+  uint64_t line = 0;
+  std::string msg;
+  const uint64_t E = tgb::parse_edge_list_device(buf.p, len, pairs, s, &line, &msg);
+  if (line) throw ParseFailure{line, msg};
+  return E;
+}
+
+template <class F>
+tg_status parse_guard(uint64_t* err_line, F&& f) {
+  if (err_line) *err_line = 0;
+  try {
+    return guard([&] { f(); });
+  } catch (const ParseFailure& e) {
+    if (err_line) *err_line = e.line;
+    t_last_error = e.msg;
+    return TG_ERR_PARSE;
+  }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* tg_last_error(void) { return t_last_error.c_str(); }
@@ -428,6 +482,7 @@ const char* tg_status_string(tg_status s) {
     case TG_ERR_OOM: return "out of device memory";
     case TG_ERR_CAPACITY: return "output capacity too small";
     case TG_ERR_INTERNAL: return "internal error";
+    case TG_ERR_PARSE: return "parse error";
   }
   return "unknown status";
 }
@@ -455,6 +510,84 @@ tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pa
     }
     *out = g;
   });
+}
+
+tg_status tg_graph_from_text(int device, const char* text, uint64_t len, uint64_t n_override,
+                             tg_graph** out, uint64_t* err_line) {
+  return parse_guard(err_line, [&] {
+    TG_REQUIRE(out != nullptr, "null output handle");
+    TG_REQUIRE(text != nullptr || len == 0, "null text");
+    tg_graph* g = new_graph(device);
+    try {
+      DBuf<uint32_t> pairs;
+      const uint64_t E = parse_text(text, len, pairs, g->stream);
+      tgb::build_graph_device(pairs.p, E, n_override, g->g, g->stream);
+      sync(g);
+    } catch (...) {
+      tg_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+tg_status tg_parse_edge_list(int device, const char* text, uint64_t len, uint32_t* pairs,
+                             uint64_t capacity, uint64_t* num_pairs, uint64_t* err_line) {
+  tg_status cap_status = TG_OK;
+  tg_status st = parse_guard(err_line, [&] {
+    TG_REQUIRE(num_pairs != nullptr, "null output");
+    TG_REQUIRE(text != nullptr || len == 0, "null text");
+    int count = 0;
+    TG_CUDA(cudaGetDeviceCount(&count));
+    TG_REQUIRE(device >= 0 && device < count, "invalid CUDA device ordinal");
+    TG_CUDA(cudaSetDevice(device));
+    cudaStream_t s;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    try {
+      DBuf<uint32_t> d;
+      const uint64_t E = parse_text(text, len, d, s);
+      *num_pairs = E;
+      if (pairs && E)
+        TG_CUDA(cudaMemcpyAsync(pairs, d.p, 8 * std::min(E, capacity),
+                                is_device_ptr(pairs) ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyDeviceToHost, s));
+      d.release();
+      TG_CUDA(cudaStreamSynchronize(s));
+      if (pairs && capacity < E) cap_status = TG_ERR_CAPACITY;  // NULL: size query
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      throw;
+    }
+    TG_CUDA(cudaStreamDestroy(s));
+  });
+  if (st == TG_OK && cap_status != TG_OK) {
+    t_last_error = "pair capacity smaller than the edge count";
+    return cap_status;
+  }
+  return st;
+}
+
+tg_status tg_write_edge_list(tg_graph* g, char* out, uint64_t capacity, uint64_t* len) {
+  tg_status cap_status = TG_OK;
+  tg_status st = guard([&] {
+    enter(g);
+    TG_REQUIRE(len != nullptr, "null output");
+    DBuf<char> d;
+    const uint64_t L = tgb::write_edge_list_device(g->g, d, g->stream);
+    *len = L;
+    if (out && L)
+      TG_CUDA(cudaMemcpyAsync(out, d.p, std::min(L, capacity),
+                              is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              g->stream));
+    sync(g);
+    if (out && capacity < L) cap_status = TG_ERR_CAPACITY;
+  });
+  if (st == TG_OK && cap_status != TG_OK) {
+    t_last_error = "text capacity smaller than the edge list";
+    return cap_status;
+  }
+  return st;
 }
 
 tg_status tg_graph_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,
@@ -534,12 +667,34 @@ tg_status tg_set_stream(tg_graph* g, void* stream) {
   });
 }
 
+tg_status tg_set_order(tg_graph* g, int32_t kind, uint64_t seed) {
+  return guard([&] {
+    enter(g);
+    apply_order(g, kind, seed);
+  });
+}
+
+tg_status tg_coreness(tg_graph* g, uint64_t* core) {
+  return guard([&] {
+    enter(g);
+    const uint64_t n = g->g.n;
+    TG_REQUIRE(core != nullptr || n == 0, "null core output");
+    if (!n) return;
+    DBuf<uint32_t> d(n, g->stream);
+    tgb::coreness_device(g->g, d.p, g->stream);
+    std::vector<uint32_t> h(n);
+    download(h.data(), d.p, n, g->stream);
+    sync(g);
+    for (uint64_t v = 0; v < n; ++v) core[v] = h[v];
+  });
+}
+
 tg_status tg_compute_order(tg_graph* g, uint32_t* rank) {
   return guard([&] {
     enter(g);
     TG_REQUIRE(rank != nullptr || g->g.n == 0, "null rank output");
     DBuf<uint32_t> d(g->g.n ? g->g.n : 1, g->stream);
-    tgb::degree_rank(g->g, d.p, g->stream);
+    tgb::order_rank(g->g, d.p, g->stream);
     download(rank, d.p, g->g.n, g->stream);
     sync(g);
   });
@@ -599,6 +754,15 @@ tg_status tg_count(tg_graph* g, uint64_t* total) {
   });
 }
 
+tg_status tg_count_node_iterator_pp(tg_graph* g, int32_t use_intersection, uint64_t* total) {
+  (void)use_intersection;  // same count either way (sequential.hpp:58-66)
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(total != nullptr, "null output");
+    *total = tgb::node_iterator_pp_device(g->g, g->stream);
+  });
+}
+
 tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total, tg_rank_stats* per_rank,
                         uint32_t* boundaries_out, uint64_t* node_counts, uint32_t* triangles,
                         uint64_t capacity, uint64_t* num_triangles) {
@@ -616,15 +780,24 @@ tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total, tg_r
       tally.alloc(n ? n : 1, s);
       tally.zero();
     }
+    // listing straight into a caller's DEVICE buffer when it holds all T
+    // triples (no staging copy: C4's 1.6e9 triangles are 19.7 GB)
+    uint32_t* list_out = nullptr;
+    bool direct = false;
     if (cfg->collect_triangles) {
       TG_REQUIRE(num_triangles != nullptr, "collect_triangles needs num_triangles");
       cap = seq_count(g);  // exact size first (ListSink holds T triples)
-      tri.alloc(3 * (cap ? cap : 1), s);
+      direct = triangles != nullptr && is_device_ptr(triangles) && capacity >= cap;
+      if (direct) {
+        list_out = triangles;
+      } else {
+        tri.alloc(3 * (cap ? cap : 1), s);
+        list_out = tri.p;
+      }
       cursor.alloc(1, s);
       cursor.zero();
     }
-    EngineResult R = run(g, *cfg, cfg->track_nodes ? tally.p : nullptr,
-                         cfg->collect_triangles ? tri.p : nullptr,
+    EngineResult R = run(g, *cfg, cfg->track_nodes ? tally.p : nullptr, list_out,
                          cfg->collect_triangles ? cursor.p : nullptr, cap);
     if (total) *total = R.total;
     if (per_rank) std::memcpy(per_rank, R.per_rank.data(), R.per_rank.size() * sizeof(tg_rank_stats));
@@ -632,7 +805,13 @@ tg_status tg_run_engine(tg_graph* g, const tg_config* cfg, uint64_t* total, tg_r
     if (cfg->track_nodes) download(node_counts, (const uint64_t*)tally.p, n, s);
     if (cfg->collect_triangles) {
       *num_triangles = R.total;
-      if (triangles) download(triangles, tri.p, 3 * std::min<uint64_t>(R.total, capacity), s);
+      if (triangles && !direct) {
+        const uint64_t words = 3 * std::min<uint64_t>(R.total, capacity);
+        if (words)
+          TG_CUDA(cudaMemcpyAsync(triangles, tri.p, words * 4,
+                                  is_device_ptr(triangles) ? cudaMemcpyDeviceToDevice
+                                                           : cudaMemcpyDeviceToHost, s));
+      }
       if (capacity < R.total) cap_status = TG_ERR_CAPACITY;
     }
     sync(g);
@@ -659,6 +838,8 @@ tg_status tg_approx_count(tg_graph* g, uint64_t p, int32_t engine, double q, uin
     c.sparsify = engine == TG_ENGINE_AOP ? TG_SPARSIFY_PER_PARTITION : TG_SPARSIFY_GLOBAL;
     c.sparsify_q = q;
     c.sparsify_seed = seed;
+    c.order_set = 1;  // the default EngineConfig::order (engines.hpp:274)
+    c.order = TG_ORDER_BY_DEGREE;
     EngineResult R = run(g, c, nullptr, nullptr, nullptr, 0);
     *estimate = (double)R.total / (q * q * q);
   });
@@ -694,6 +875,7 @@ tg_status tg_variance_report(tg_graph* g, const uint32_t* boundaries, uint64_t p
     enter(g);
     TG_REQUIRE(boundaries && p >= 1 && out3 && var2, "invalid argument");
     cudaStream_t s = g->stream;
+    apply_order(g, TG_ORDER_BY_DEGREE, 0);  // sparsify.hpp:123-124
     ensure_eff(g);
     const std::vector<uint32_t> b = plan_for(g, TG_COST_DPD, p, boundaries);
     const uint64_t n = g->g.n, m = g->g.m2 / 2;

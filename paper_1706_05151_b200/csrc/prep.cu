@@ -189,7 +189,7 @@ void launch_orient(const DevGraph& g, uint32_t vlo, uint32_t vhi, uint64_t* cnt,
                    uint32_t* eff, cudaStream_t s) {
   uint64_t rows = vhi - vlo;
   unsigned grid = grid_for(rows * G, 256, 148u * 32u);
-  k_orient<G, 0><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, vlo, vhi, cnt, nullptr);
+  k_orient<G, 0><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), vlo, vhi, cnt, nullptr);
   TG_CHECK_LAUNCH();
   ++g_launches;
   // exclusive scan into off_out[0..rows]
@@ -199,7 +199,7 @@ void launch_orient(const DevGraph& g, uint32_t vlo, uint32_t vhi, uint64_t* cnt,
       return cub::DeviceScan::InclusiveSum(t, b, cnt, off_out + 1, (int64_t)rows, s);
     });
     g_launches += 2;  // CUB decoupled look-back scan: init + scan kernels
-    k_orient<G, 1><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, vlo, vhi, off_out, eff);
+    k_orient<G, 1><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), vlo, vhi, off_out, eff);
     TG_CHECK_LAUNCH();
     ++g_launches;
   }
@@ -208,7 +208,7 @@ void launch_orient(const DevGraph& g, uint32_t vlo, uint32_t vhi, uint64_t* cnt,
 template <int G>
 void launch_orient_gappy(const DevGraph& g, uint64_t* desc, uint32_t* eff, cudaStream_t s) {
   unsigned grid = grid_for(g.n * G, 256, 148u * 32u);
-  k_orient<G, 2><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, 0, (uint32_t)g.n, desc, eff);
+  k_orient<G, 2><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), 0, (uint32_t)g.n, desc, eff);
   TG_CHECK_LAUNCH();
   ++g_launches;
 }
@@ -664,6 +664,7 @@ __global__ void k_cost_simple(const uint64_t* __restrict__ edesc, const uint32_t
 
 // DPD (partition.hpp:60-69): sum_{u in N_v} (h_v + h_u)
 // NOV (partition.hpp:70-81): sum_{u in adj(v), u precedes v} (h_v + h_u)
+// `key` is the order key (degree, or the rank of a non-degree order).
 template <bool NOV>
 __global__ void __launch_bounds__(256)
 k_cost_sum(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
@@ -852,22 +853,22 @@ static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t mwords = g.m2 / 32 + 8;
   DBuf<uint32_t> kmask(2 * mwords, s);
   kmask.zero();
-  k_orient_tiles<0, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, cnt.p,
+  k_orient_tiles<0, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, g.n, cnt.p,
                                                       nullptr, nullptr, ctr.p, bigq.p, ctr.p + 2,
                                                       kmask.p, nullptr);
   TG_CHECK_LAUNCH();
-  k_orient_big<false, CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p, ctr.p + 2, cnt.p,
+  k_orient_big<false, CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq.p, ctr.p + 2, cnt.p,
                                               nullptr, nullptr, kmask.p + mwords);
   TG_CHECK_LAUNCH();
   TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
   cub_run(s, [&](void* t, size_t& b) {
     return cub::DeviceScan::InclusiveSum(t, b, cnt.p, out.off.p + 1, (int64_t)g.n, s);
   });
-  k_orient_tiles<1, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n, out.off.p,
+  k_orient_tiles<1, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, g.n, out.off.p,
                                                      out.desc.p, out.data.p, ctr.p + 1, nullptr,
                                                      nullptr, kmask.p, cnt.p);
   TG_CHECK_LAUNCH();
-  k_orient_big<true, CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p, ctr.p + 2,
+  k_orient_big<true, CODED><<<148 * 8, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq.p, ctr.p + 2,
                                              out.off.p, out.desc.p, out.data.p, kmask.p + mwords);
   TG_CHECK_LAUNCH();
   g_launches += 6;  // count, big count, scan (init + sweep), fill, big fill
@@ -880,11 +881,11 @@ static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
   DBuf<uint32_t> bigq(g.n, s);
   DBuf<unsigned long long> ctr(6, s);  // tile counter + k_orient_big1's counters
   ctr.zero();
-  k_orient_tiles<2, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, g.n,
+  k_orient_tiles<2, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, g.n,
                                                          nullptr, out.desc.p, out.data.p, ctr.p,
                                                          bigq.p, ctr.p + 1, nullptr, nullptr);
   TG_CHECK_LAUNCH();
-  k_orient_big1<CODED><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, g.dcode.p, bigq.p, g.n,
+  k_orient_big1<CODED><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq.p, g.n,
                                                ctr.p, g.m2, out.desc.p, out.data.p);
   TG_CHECK_LAUNCH();
   g_launches += 2;
@@ -908,7 +909,7 @@ void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   if (out.desc.n < g.n) out.desc.alloc(g.n, s);
   if (out.data.n < slots + kQuadPad) out.data.alloc(slots + kQuadPad, s);
   out.off.release();
-  if (g.n > (32ull << 20)) orient_onepass<true>(g, out, s);
+  if (order_coded(g)) orient_onepass<true>(g, out, s);
   else orient_onepass<false>(g, out, s);
 }
 
@@ -930,7 +931,7 @@ void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s) {
     return;
   }
   // 1-byte degree codes once the 4-byte degrees would not stay in L2
-  if (g.n > (32ull << 20)) orient_tiles<true>(g, out, s);
+  if (order_coded(g)) orient_tiles<true>(g, out, s);
   else orient_tiles<false>(g, out, s);
 }
 
@@ -1016,9 +1017,9 @@ void node_costs_device(const DevGraph& g, const DevEff& eff, int kind, uint64_t*
   if (kind == TG_COST_DPD || kind == TG_COST_NOV) {
     unsigned grid = grid_for(g.n * 32, 256, 148u * 32u);
     if (kind == TG_COST_DPD)
-      k_cost_sum<false><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, ev, g.n, d_f);
+      k_cost_sum<false><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), ev, g.n, d_f);
     else
-      k_cost_sum<true><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, g.deg.p, ev, g.n, d_f);
+      k_cost_sum<true><<<grid, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), ev, g.n, d_f);
   } else {
     k_cost_simple<<<grid_for(g.n, 256), 256, 0, s>>>(eff.desc.p, g.deg.p, g.n, kind, d_f);
   }

@@ -86,7 +86,22 @@ struct DevGraph {
   DBuf<uint32_t> deg;      // n
   DBuf<uint8_t> dcode;     // n: monotone 1-byte degree code (orientation)
   uint64_t big_entries = 0;  // sum of degrees of the orientation's hub vertices
+  // Total order of the orientation (order.hpp:17-35).  ByDegree keys on
+  // `deg` (or `dcode`); every other kind keys on okey = its rank array, so
+  // precedes(v, u) = okey[v] < okey[u] through the same kernels.
+  int order = TG_ORDER_BY_DEGREE;
+  uint64_t order_seed = 0;
+  DBuf<uint32_t> okey;     // n (non-degree orders only)
 };
+
+// Order key array and key kind used by the orientation kernels.
+inline const uint32_t* order_key(const DevGraph& g) {
+  return g.order == TG_ORDER_BY_DEGREE ? g.deg.p : g.okey.p;
+}
+// 1-byte degree codes once the 4-byte degrees would not stay in L2.
+inline bool order_coded(const DevGraph& g) {
+  return g.order == TG_ORDER_BY_DEGREE && g.n > (32ull << 20);
+}
 
 // Monotone 1-byte code of a degree: exact below 240, then one bucket per
 // doubling.  code(a) < code(b) implies a < b; equal codes below 240 imply
@@ -155,6 +170,25 @@ void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
 uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s);
 void degree_rank(const DevGraph& g, uint32_t* d_rank, cudaStream_t s);
 
+// ---- edge-list text (io.cu, io.hpp:18-64) ----
+// parse_edge_list over a device text buffer padded with >= 16 zero bytes
+// past `len` (16-byte aligned).  Returns the pair count (pairs: interleaved
+// u, v in file order); on a ParseError returns 0 with *err_line = the
+// 1-based line and *err_msg = "line N: ..." (io.hpp:18-22).
+uint64_t parse_edge_list_device(const char* d_text, uint64_t len, DBuf<uint32_t>& pairs,
+                                cudaStream_t s, uint64_t* err_line, std::string* err_msg);
+// write_edge_list: "u v\n" for every edge u < v; returns the byte length.
+uint64_t write_edge_list_device(const DevGraph& g, DBuf<char>& out, cudaStream_t s);
+
+// ---- orders (order.cu, order.hpp:39-128) ----
+// Switch g's orientation order to OrderKind{kind, seed}: builds g.okey
+// (the rank array) for non-degree kinds.
+void set_order(DevGraph& g, int kind, uint64_t seed, cudaStream_t s);
+// rank (n) of g's current order.
+void order_rank(const DevGraph& g, uint32_t* d_rank, cudaStream_t s);
+// coreness (order.hpp:39-83): core numbers (n), parallel peeling.
+void coreness_device(const DevGraph& g, uint32_t* d_core, cudaStream_t s);
+
 // ---- costs / plan (costs.cu) ----
 // f (n), prefix (n) on device.
 void node_costs_device(const DevGraph& g, const DevEff& eff, int kind, uint64_t* d_f,
@@ -202,7 +236,9 @@ void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
 void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,
                        cudaStream_t s);
 
-// ---- analytics.cu (sequential.hpp:108-122, sparsify.hpp:113-155) ----
+// ---- analytics.cu (sequential.hpp:48-70, 108-122, sparsify.hpp:113-155) ----
+// count_node_iterator_pp under g's current order (host result).
+uint64_t node_iterator_pp_device(const DevGraph& g, cudaStream_t s);
 // d_up (n+1): exclusive prefix of #neighbours above v (edges() order).
 void upper_offsets(const DevGraph& g, uint64_t* d_up, cudaStream_t s);
 // bump t_e of the three edges of each listed triple (ascending ids) into

@@ -21,7 +21,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from ._lib import TgConfig, TgRankStats, check, lib
+from ._lib import ParseError, TgConfig, TgRankStats, check, lib  # noqa: F401 (ParseError re-exported)
 
 NodeId = np.uint32
 
@@ -154,6 +154,113 @@ def build_graph_from_pointer(ptr: int, num_pairs: int, n_override: int = 0,
     return Graph(h, device)
 
 
+class OrderTag(enum.IntEnum):  # order.hpp:19 OrderKind::Tag
+    ById = 0
+    ByDegree = 1
+    ByRandom = 2
+    ByCoreness = 3
+
+
+@dataclass(frozen=True)
+class OrderKind:  # order.hpp:17-28
+    tag: OrderTag = OrderTag.ByDegree
+    seed: int = 0
+
+    @staticmethod
+    def by_id() -> "OrderKind":
+        return OrderKind(OrderTag.ById, 0)
+
+    @staticmethod
+    def by_degree() -> "OrderKind":
+        return OrderKind(OrderTag.ByDegree, 0)
+
+    @staticmethod
+    def by_random(seed: int) -> "OrderKind":
+        return OrderKind(OrderTag.ByRandom, int(seed))
+
+    @staticmethod
+    def by_coreness() -> "OrderKind":
+        return OrderKind(OrderTag.ByCoreness, 0)
+
+
+_ORDER_NAMES = {"by_id": OrderTag.ById, "id": OrderTag.ById, "ById": OrderTag.ById,
+                "by_degree": OrderTag.ByDegree, "degree": OrderTag.ByDegree,
+                "ByDegree": OrderTag.ByDegree, "by_random": OrderTag.ByRandom,
+                "random": OrderTag.ByRandom, "ByRandom": OrderTag.ByRandom,
+                "by_coreness": OrderTag.ByCoreness, "coreness": OrderTag.ByCoreness,
+                "ByCoreness": OrderTag.ByCoreness}
+
+
+def _order(kind, seed: int = 0) -> OrderKind:
+    """OrderKind from an OrderKind, an OrderTag or a name (cli.hpp:67-72
+    spellings: id, degree, random, coreness)."""
+    if kind is None:
+        return OrderKind.by_degree()
+    if isinstance(kind, OrderKind):
+        return kind
+    if isinstance(kind, str):
+        if kind not in _ORDER_NAMES:
+            raise ValueError(f"unknown ordering '{kind}'")
+        kind = _ORDER_NAMES[kind]
+    return OrderKind(OrderTag(int(kind)), int(seed) if int(kind) == OrderTag.ByRandom else 0)
+
+
+def _use_order(g: "Graph", kind) -> None:
+    o = _order(kind)
+    check(lib().tg_set_order(g._h, int(o.tag), int(o.seed)))
+
+
+# ---------------------------------------------------------------- edge lists
+
+
+def _text_ptr(text):
+    """(pointer, length, keep-alive) of bytes / str / a CUDA uint8 tensor."""
+    if hasattr(text, "data_ptr"):
+        return C.c_void_p(text.data_ptr()), int(text.numel() * text.element_size()), text
+    if isinstance(text, str):
+        text = text.encode("latin-1")
+    buf = np.frombuffer(bytes(text), dtype=np.uint8)
+    return (_p(buf) if buf.size else None), int(buf.size), buf
+
+
+def parse_edge_list(text, device: int = 0) -> np.ndarray:
+    """io.hpp:24-50 on the device: (E, 2) uint32 pairs in file order.  Raises
+    ParseError (with ``.line``) like the reference."""
+    ptr, n, keep = _text_ptr(text)
+    cnt, line = C.c_uint64(), C.c_uint64()
+    if isinstance(keep, np.ndarray):  # host text: at most one edge per line
+        cap = int(np.count_nonzero(keep == 10)) + 1
+    else:  # device text: ask for the count first
+        check(lib().tg_parse_edge_list(device, ptr, n, None, 0, C.byref(cnt), C.byref(line)),
+              line.value)
+        cap = cnt.value
+    out = np.zeros((max(cap, 1), 2), dtype=np.uint32)
+    check(lib().tg_parse_edge_list(device, ptr, n, _p(out), cap, C.byref(cnt), C.byref(line)),
+          line.value)
+    del keep
+    return out[: cnt.value]
+
+
+def build_graph_from_text(text, n_override: int = 0, device: int = 0) -> "Graph":
+    """build_graph(parse_edge_list(text), n_override) with both on the device
+    (cli.hpp:81-88 --input)."""
+    ptr, n, keep = _text_ptr(text)
+    h, line = C.c_void_p(), C.c_uint64()
+    check(lib().tg_graph_from_text(device, ptr, n, n_override, C.byref(h), C.byref(line)),
+          line.value)
+    del keep
+    return Graph(h, device)
+
+
+def write_edge_list(g: "Graph") -> bytes:
+    """io.hpp:52-64 on the device: "u v\n" for every edge u < v."""
+    n = C.c_uint64()
+    check(lib().tg_write_edge_list(g._h, None, 0, C.byref(n)))
+    buf = np.zeros(max(n.value, 1), dtype=np.uint8)
+    check(lib().tg_write_edge_list(g._h, _p(buf), n.value, C.byref(n)))
+    return buf[: n.value].tobytes()
+
+
 @dataclass
 class OrderRank:  # order.hpp:31-35
     rank: np.ndarray
@@ -162,11 +269,18 @@ class OrderRank:  # order.hpp:31-35
         return bool(self.rank[u] < self.rank[v])
 
 
-def compute_order(g: Graph, kind: str = "by_degree") -> OrderRank:
-    """order.hpp:85-128, ByDegree only (the degree order is the north_star
-    path and provably optimal)."""
-    if kind not in ("by_degree", "ByDegree"):
-        raise ValueError("only OrderKind::by_degree() is supported on the device")
+def coreness(g: Graph) -> np.ndarray:
+    """order.hpp:39-83 core numbers (device peeling), uint64[n]."""
+    n = g.num_nodes()
+    c = np.zeros(max(n, 1), dtype=np.uint64)
+    check(lib().tg_coreness(g._h, _p(c)))
+    return c[:n]
+
+
+def compute_order(g: Graph, kind=None) -> OrderRank:
+    """order.hpp:85-128 compute_order(g, kind) for every OrderKind (default
+    by_degree, the hot path).  ``kind``: OrderKind, OrderTag or a name."""
+    _use_order(g, kind)
     n = g.num_nodes()
     r = np.zeros(max(n, 1), dtype=np.uint32)
     check(lib().tg_compute_order(g._h, _p(r)))
@@ -191,8 +305,10 @@ class EffectiveAdjacency:  # effective.hpp:17-35
         return int(self.offsets[v + 1] - self.offsets[v])
 
 
-def effective_adjacency(g: Graph) -> EffectiveAdjacency:
-    """effective.hpp:37-52 under the degree order (oriented on the device)."""
+def effective_adjacency(g: Graph, order=None) -> EffectiveAdjacency:
+    """effective.hpp:37-52 under ``order`` (default by_degree), oriented on
+    the device."""
+    _use_order(g, order)
     n, m = g._info()
     off = np.zeros(n + 1, dtype=np.uint64)
     eff = np.zeros(max(m, 1), dtype=np.uint32)
@@ -200,15 +316,28 @@ def effective_adjacency(g: Graph) -> EffectiveAdjacency:
     return EffectiveAdjacency(off, eff[:m])
 
 
-def count_node_iterator_n(g: Graph) -> int:
-    """sequential.hpp:74-91 count over effective_adjacency(g, by_degree)."""
+def count_node_iterator_n(g: Graph, order=None) -> int:
+    """sequential.hpp:74-91 count over effective_adjacency(g, order)
+    (default by_degree)."""
+    _use_order(g, order)
     t = C.c_uint64()
     check(lib().tg_count(g._h, C.byref(t)))
     return t.value
 
 
-def ordering_cost(g: Graph) -> int:
-    """sequential.hpp:95-104 under the degree order: W = sum_v d_v * h_v."""
+def count_node_iterator_pp(g: Graph, order=None, use_intersection: bool = False) -> int:
+    """sequential.hpp:48-70 NodeIterator++ (the paper's baseline) under
+    ``order`` (default by_degree), on the device."""
+    _use_order(g, order)
+    t = C.c_uint64()
+    check(lib().tg_count_node_iterator_pp(g._h, int(bool(use_intersection)), C.byref(t)))
+    return t.value
+
+
+def ordering_cost(g: Graph, order=None) -> int:
+    """sequential.hpp:95-104: W = sum_v d_v * h_v under ``order`` (default
+    by_degree)."""
+    _use_order(g, order)
     t = C.c_uint64()
     check(lib().tg_ordering_cost(g._h, C.byref(t)))
     return t.value
@@ -223,8 +352,10 @@ class CostVector:  # partition.hpp:38-43
         return int(self.prefix[-1]) if self.prefix.size else 0
 
 
-def node_costs(g: Graph, kind: CostKind) -> CostVector:
-    """partition.hpp:45-91 (DpdVariant::EffectiveOnly)."""
+def node_costs(g: Graph, kind: CostKind, order=None) -> CostVector:
+    """partition.hpp:45-91 (DpdVariant::EffectiveOnly) over
+    effective_adjacency(g, order) (default by_degree)."""
+    _use_order(g, order)
     n = g.num_nodes()
     f = np.zeros(max(n, 1), dtype=np.uint64)
     pre = np.zeros(max(n, 1), dtype=np.uint64)
@@ -253,10 +384,12 @@ class PartitionPlan:  # partition.hpp:95-110
         return int(np.searchsorted(inner, v, side="right"))
 
 
-def compute_boundaries(g: Graph, kind: CostKind, p: int) -> PartitionPlan:
-    """partition.hpp:116-141 over node_costs(g, kind): exact 128-bit search."""
+def compute_boundaries(g: Graph, kind: CostKind, p: int, order=None) -> PartitionPlan:
+    """partition.hpp:116-141 over node_costs(g, kind, order): exact 128-bit
+    search."""
     if p < 1:
         raise ValueError("compute_boundaries: p must be >= 1")
+    _use_order(g, order)
     b = np.zeros(p + 1, dtype=np.uint32)
     check(lib().tg_compute_boundaries(g._h, int(kind), p, _p(b)))
     return PartitionPlan(b)
@@ -283,7 +416,7 @@ class EngineConfig:  # engines.hpp:270-280
     engine: EngineKind = EngineKind.Aop
     ranks: int = 1
     cost: CostKind = CostKind.Dpd
-    order: str = "by_degree"
+    order: object = field(default_factory=OrderKind.by_degree)  # OrderKind (or a name)
     mode: ExecMode = ExecMode.Interleaved
     track_nodes: bool = False
     collect_triangles: bool = False
@@ -313,9 +446,11 @@ class RunReport:  # engines.hpp:289-298
 
 
 def _cfg(cfg: EngineConfig):
-    if cfg.order not in ("by_degree", "ByDegree"):
-        raise ValueError("only OrderKind::by_degree() is supported on the device")
+    o = _order(cfg.order)
     c = TgConfig()
+    c.order_set = 1
+    c.order = int(o.tag)
+    c.order_seed = int(o.seed)
     c.engine = int(cfg.engine)
     c.cost = int(cfg.cost)
     c.ranks = int(cfg.ranks)
@@ -336,10 +471,12 @@ def _cfg(cfg: EngineConfig):
     return c, keep
 
 
-def run_engine(g: Graph, cfg: EngineConfig) -> RunReport:
+def run_engine(g: Graph, cfg: EngineConfig, triangles_out=None) -> RunReport:
     """engines.hpp:335-418.  ``triangles_list`` rows are normalised to
     ascending ids (engines.hpp:313-319); row order is unspecified, as in the
-    reference (compare sorted)."""
+    reference (compare sorted).  ``triangles_out``: optional device buffer
+    (a CUDA tensor of >= 3*T int32/uint32 words, e.g. shape (T, 3)) that the
+    listing kernels write in place; ``triangles_list`` is then a view of it."""
     if cfg.engine != EngineKind.Sequential and int(cfg.ranks) < 1:
         raise ValueError("run_engine: ranks must be >= 1")
     c, keep = _cfg(cfg)
@@ -349,11 +486,19 @@ def run_engine(g: Graph, cfg: EngineConfig) -> RunReport:
     b = np.zeros(p + 1, dtype=np.uint32)
     total = C.c_uint64()
     tv = np.zeros(max(n, 1), dtype=np.uint64) if cfg.track_nodes else None
-    cap = count_node_iterator_n(g) if cfg.collect_triangles else 0
-    tri = np.zeros((max(cap, 1), 3), dtype=np.uint32) if cfg.collect_triangles else None
+    if triangles_out is not None and cfg.collect_triangles:
+        if triangles_out.element_size() != 4 or not triangles_out.is_contiguous():
+            raise ValueError("triangles_out must be a contiguous 32-bit device buffer")
+        tri = None
+        cap = triangles_out.numel() // 3
+        tri_ptr = C.c_void_p(triangles_out.data_ptr())
+    else:
+        cap = count_node_iterator_n(g, cfg.order) if cfg.collect_triangles else 0
+        tri = np.zeros((max(cap, 1), 3), dtype=np.uint32) if cfg.collect_triangles else None
+        tri_ptr = _p(tri)
     ntri = C.c_uint64()
     check(lib().tg_run_engine(g._h, C.byref(c), C.byref(total), C.cast(stats, C.c_void_p), _p(b),
-                              _p(tv), _p(tri), cap, C.byref(ntri)))
+                              _p(tv), tri_ptr, cap, C.byref(ntri)))
     del keep
     rep = RunReport(engine=EngineKind(cfg.engine), ranks=p, cost=CostKind(cfg.cost),
                     total=total.value, boundaries=b)
@@ -362,7 +507,10 @@ def run_engine(g: Graph, cfg: EngineConfig) -> RunReport:
     if cfg.track_nodes:
         rep.node_counts = tv[:n]
     if cfg.collect_triangles:
-        rep.triangles_list = tri[: ntri.value]
+        if tri is None:
+            rep.triangles_list = triangles_out.view(-1)[: 3 * ntri.value].view(-1, 3)
+        else:
+            rep.triangles_list = tri[: ntri.value]
     return rep
 
 
@@ -401,7 +549,9 @@ def approx_count(g: Graph, p: int, engine: EngineKind, q: float, seed: int,
 def per_edge_triangle_counts(g: Graph) -> np.ndarray:
     """sequential.hpp:108-122: t_e for every edge, in Graph::edges() order
     (u < v; graph.hpp:40-46).  The reference returns a map keyed by (u, v);
-    pair it with ``Graph.edges()``."""
+    pair it with ``Graph.edges()``.  t_e does not depend on the order; the
+    degree order (as cli.hpp:312-313) keeps the listing short."""
+    _use_order(g, None)
     m = g.num_edges()
     te = np.zeros(max(m, 1), dtype=np.uint64)
     check(lib().tg_per_edge_triangle_counts(g._h, _p(te)))

@@ -51,3 +51,17 @@ def next_golden():
     """sparsification, per-edge counts, variance report."""
     with open(os.path.join(GOLDEN, "reference_next.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def orders_golden():
+    """Every OrderKind (order.hpp:17-128) through the reference."""
+    with open(os.path.join(GOLDEN, "reference_orders.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def io_golden():
+    """parse_edge_list / write_edge_list (io.hpp:18-64) through the reference."""
+    with open(os.path.join(GOLDEN, "reference_io.json")) as f:
+        return json.load(f)

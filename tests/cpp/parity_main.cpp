@@ -96,6 +96,77 @@ int main(int argc, char** argv) {
     auto vr = variance_report(g5(), plan, 0.5);
     CHECK(vr.triangles == 2 && vr.k == 1 && vr.k_prime == 1 && vr.var == 16.0);
   }
+  {  // test_io.cpp:12-24 parse_edge_list basics
+    auto e = parse_edge_list("0 1\n1 2\n");
+    CHECK(e.size() == 2 && e[0] == (std::pair<NodeId, NodeId>{0, 1}) &&
+          e[1] == (std::pair<NodeId, NodeId>{1, 2}));
+    auto c = parse_edge_list("# comment\n3 4\n");
+    CHECK(c.size() == 1 && c[0] == (std::pair<NodeId, NodeId>{3, 4}));
+    CHECK(parse_edge_list("").empty());
+    CHECK(parse_edge_list("\n  \n# only comments\n").empty());
+  }
+  {  // test_io.cpp:26-35 errors carry line numbers
+    bool threw = false;
+    try {
+      parse_edge_list("0 x\n");
+    } catch (const ParseError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    std::size_t line = 0;
+    try {
+      parse_edge_list("0 1\n\n2 y\n");
+    } catch (const ParseError& e) {
+      line = e.line;
+    }
+    CHECK(line == 3);
+    threw = false;
+    try {
+      parse_edge_list("1 2 3\n");
+    } catch (const ParseError& e) {
+      threw = std::string(e.what()) == "line 1: trailing token '3'";
+    }
+    CHECK(threw);
+  }
+  {  // test_io.cpp:37-46 round trip
+    auto g = g5();
+    auto text = write_edge_list(g);
+    std::size_t nl = 0;
+    for (char ch : text) nl += ch == '\n';
+    CHECK(nl == 6);
+    auto g2 = build_graph(parse_edge_list(text));
+    CHECK(g2.num_nodes() == g.num_nodes() && g2.num_edges() == g.num_edges());
+    CHECK(write_edge_list(g2) == text);
+    CHECK(write_edge_list(build_graph_from_text(text)) == text);
+    CHECK(write_edge_list(build_graph({})).empty());
+  }
+  {  // test_graph.cpp:51-55 coreness
+    CHECK((coreness(build_graph({{0, 1}, {0, 2}, {1, 2}})) == std::vector<std::size_t>{2, 2, 2}));
+    CHECK((coreness(build_graph({{0, 1}, {1, 2}})) == std::vector<std::size_t>{1, 1, 1}));
+    CHECK((coreness(g5()) == std::vector<std::size_t>{2, 2, 2, 2, 1}));
+  }
+  {  // test_graph.cpp:67-71, :79-91, :111-116; test_sequential.cpp:84-87
+    auto g = g5();
+    auto id = compute_order(g, OrderKind::by_id());
+    for (NodeId v = 0; v < 5; ++v) CHECK(id.rank[v] == v);
+    auto a = compute_order(g, OrderKind::by_random(42));
+    auto b = compute_order(g, OrderKind::by_random(42));
+    CHECK(a.rank == b.rank);
+    auto eff = effective_adjacency(g, OrderKind::by_id());
+    CHECK(eff.effdeg(3) == 1 && eff.entries[eff.offsets[3]] == 4 && eff.effdeg(4) == 0);
+    CHECK(ordering_cost(g, OrderKind::by_id()) == 16);
+    CHECK(ordering_cost(g) == 14);
+    for (auto kind : {OrderKind::by_id(), OrderKind::by_degree(), OrderKind::by_random(3),
+                      OrderKind::by_coreness()}) {
+      CHECK(count_node_iterator_n(g, kind) == 2);
+      CHECK(count_node_iterator_pp(g, kind) == 2);          // test_sequential.cpp:20-31
+      CHECK(count_node_iterator_pp(g, kind, true) == 2);
+      CHECK(effective_adjacency(g, kind).total_entries() == g.num_edges());
+      auto cfg = config(EngineKind::AnopSurrogate, 3);
+      cfg.order = kind;
+      CHECK(run_engine(g, cfg).total == 2);
+    }
+  }
   {  // a PA graph through every engine: totals and per-rank sums agree
     auto g = gen_pa(20000, 20, 3);
     std::uint64_t t = count_node_iterator_n(g);

@@ -5,6 +5,8 @@ oracle/_ref/libtrigraph_ref.so):
 
     python tests/golden/make_golden.py            # small fixtures (seconds)
     python tests/golden/make_golden.py --next     # only the 8(f) rows (sparsify, t_e)
+    python tests/golden/make_golden.py --orders   # only the OrderKind fixtures
+    python tests/golden/make_golden.py --io       # only the edge-list text fixtures
     python tests/golden/make_golden.py --full     # + full-size C1/C2 goldens
 
 Every number in the fixtures comes from the reference's own functions
@@ -215,6 +217,118 @@ def next_rows():
     return fx
 
 
+ORDERS = [("id", 0), ("degree", 0), ("random", 42), ("random", 43), ("coreness", 0)]
+
+
+def order_record(R: B.RefGraph, engines=(("aop", 3), ("anop-direct", 2), ("anop-surrogate", 4)),
+                 explicit=False):
+    """compute_order / coreness / effective_adjacency / count / ordering_cost
+    and run_engine under every OrderKind (order.hpp:85-128, engines.hpp:274)."""
+    g = R.csr()
+    core = R.coreness()
+    rec = {"n": g.n, "m": g.m, "adj_sha256": digest(g.adj), "coreness_sha256": digest(core),
+           "orders": []}
+    if explicit:
+        rec["coreness"] = core.tolist()
+    for order, seed in ORDERS:
+        rank = R.compute_order(order, seed)
+        eoff, eff, cnt, cost = R.effective_order(order, seed)
+        o = {"order": order, "seed": seed, "rank_sha256": digest(rank),
+             "eff_offsets_sha256": digest(eoff), "eff_sha256": digest(eff),
+             "count": cnt, "ordering_cost": cost, "engines": []}
+        if explicit:
+            o["rank"] = rank.tolist()
+            o["eff_offsets"] = eoff.tolist()
+            o["eff"] = eff.tolist()
+        for e, p in engines:
+            rep = R.run_engine_order(e, p, order, seed, track_nodes=True, collect_triangles=True)
+            o["engines"].append({
+                "engine": e, "ranks": p, "total": rep.total,
+                "boundaries": rep.boundaries[: p + 1].tolist(),
+                "triangles": rep.triangles[:p].tolist(),
+                "data_sent": rep.data_sent[:p].tolist(),
+                "data_recv": rep.data_recv[:p].tolist(),
+                "node_counts_sha256": digest(rep.node_counts),
+                "triangles_sha256": digest(rep.triangles_list)})
+        rec["orders"].append(o)
+    return rec
+
+
+def orders():
+    """Every OrderKind of the reference (order.hpp:17-128): the order-dependent
+    results on G5 (explicit), small fixtures and seeded graphs."""
+    from paper_1706_05151_b200 import trigraph as T  # generators only (host harness)
+    fx = {"g5": order_record(B.ref_fixture("g5"), explicit=True),
+          "k3_coreness": B.ref_fixture("complete", 3).coreness().tolist(),
+          "path_coreness": B.RefGraph.from_pairs([[0, 1], [1, 2]]).coreness().tolist()}
+    fx["random"] = []
+    for i in range(12):
+        n, dens, seed = 20 + 9 * i, 0.05 + 0.07 * i, 500 + i
+        rec = order_record(B.ref_random_graph(n, dens, seed))
+        rec.update({"gen": [n, dens, seed]})
+        fx["random"].append(rec)
+    fx["pa20000"] = order_record(B.ref_fixture("gen_pa", 20000, 20, 3),
+                                 engines=(("aop", 8), ("anop-surrogate", 8)))
+    pairs = T.gen_rmat(12, 8, 0.57, 0.19, 0.19, 5)
+    rec = order_record(B.RefGraph.from_pairs(pairs), engines=(("aop", 4), ("anop-surrogate", 4)))
+    rec["pairs_sha256"] = digest(np.ascontiguousarray(pairs, dtype=np.uint32))
+    fx["rmat12"] = rec
+    return fx
+
+
+def io_texts():
+    """Edge-list texts for parse_edge_list (io.hpp:24-50): the reference tests'
+    cases, the istream corner cases (signs, overflow, \\v/\\f, CRLF, NUL,
+    trailing tokens) and seeded random texts."""
+    import random
+    rng = random.Random(1706)
+    texts = [b"", b"0 1\n1 2\n", b"# comment\n3 4\n", b"\n  \n# only comments\n", b"0 x\n",
+             b"0 1\n\n2 y\n", b"1 2 3\n", b"12+3\n", b"12-3", b"-1 -2\n", b"+5 +6\r\n",
+             b" \t# x\n1 2", b"1\n2\n", b"\v1 2\n", b"1 2\v\n", b"1 2 #c\n",
+             b"4294967296 4294967297\n", b"18446744073709551615 0\n",
+             b"18446744073709551616 0\n", b"-18446744073709551615 1\n",
+             b"-18446744073709551616 1\n", b"00012 0003\n", b"1 2\x00\n", b"\r\n\r\n1\t2\r\n",
+             b"1 2\n3 4\n5 6\n7 8 x\n9 10\n", b"#\n#\n 3  4 \n\f5 6\n", b"- 1\n", b"+\n", b"1 +\n"]
+    ws = [b"", b" ", b"\t", b"  ", b"\r", b" \v", b"\f"]
+    nums = [b"0", b"1", b"42", b"+7", b"-3", b"4294967295", b"4294967296",
+            b"18446744073709551615", b"007", b"123456"]
+    for _ in range(300):
+        lines = []
+        for _ in range(rng.randint(0, 12)):
+            r = rng.random()
+            if r < 0.1:
+                lines.append(rng.choice(ws) + b"# c " + rng.choice(nums))
+            elif r < 0.15:
+                lines.append(rng.choice(ws))
+            else:
+                lines.append(rng.choice(ws) + rng.choice(nums) + rng.choice(ws[1:]) +
+                             rng.choice(nums) + rng.choice(ws) +
+                             (b" x" if rng.random() < 0.02 else b""))
+        texts.append(b"\n".join(lines) + (b"\n" if rng.random() < 0.5 else b""))
+    return texts
+
+
+def io_rows():
+    """parse_edge_list / write_edge_list (io.hpp:18-64) through the reference."""
+    from paper_1706_05151_b200 import trigraph as T  # generators only (host harness)
+    cases = []
+    for t in io_texts():
+        r = B.ref_parse_edge_list(t)
+        if isinstance(r, tuple):
+            cases.append({"text": t.decode("latin-1"), "error_line": r[0], "error": r[1]})
+        else:
+            cases.append({"text": t.decode("latin-1"), "pairs": r.reshape(-1).tolist()})
+    fx = {"parse": cases}
+    for name, R in (("g5", B.ref_fixture("g5")), ("pa20000", B.ref_fixture("gen_pa", 20000, 20, 3)),
+                    ("rmat12", B.RefGraph.from_pairs(T.gen_rmat(12, 8, 0.57, 0.19, 0.19, 5)))):
+        txt = R.write_edge_list()
+        rec = {"len": len(txt), "sha256": hashlib.sha256(txt).hexdigest(), "m": R.m, "n": R.n}
+        if name == "g5":
+            rec["text"] = txt.decode("latin-1")
+        fx["write_" + name] = rec
+    return fx
+
+
 def full():
     sys.path.insert(0, ROOT)
     from paper_1706_05151_b200 import trigraph as T  # generators only (host harness)
@@ -244,9 +358,24 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--next", action="store_true", help="only reference_next.json")
+    ap.add_argument("--orders", action="store_true", help="only reference_orders.json")
+    ap.add_argument("--io", action="store_true", help="only reference_io.json")
     a = ap.parse_args()
     if not B.ref_available():
         sys.exit("oracle/_ref not built (make -C oracle with /root/reference mounted)")
+    sys.path.insert(0, ROOT)
+    fx = io_rows()
+    with open(os.path.join(OUT, "reference_io.json"), "w") as f:
+        json.dump(fx, f, indent=0, sort_keys=True)
+    print("wrote reference_io.json")
+    if a.io:
+        sys.exit(0)
+    fx = orders()
+    with open(os.path.join(OUT, "reference_orders.json"), "w") as f:
+        json.dump(fx, f, indent=0, sort_keys=True)
+    print("wrote reference_orders.json")
+    if a.orders:
+        sys.exit(0)
     fx = next_rows()
     with open(os.path.join(OUT, "reference_next.json"), "w") as f:
         json.dump(fx, f, indent=0, sort_keys=True)

@@ -54,7 +54,12 @@ def test_host_validation_maps_to_reference_exceptions():
     with pytest.raises(ValueError):
         T._cfg(T.EngineConfig(engine=T.EngineKind.Aop, ranks=2, boundaries=[0, 1]))
     with pytest.raises(ValueError):
-        T._cfg(T.EngineConfig(order="by_id"))
+        T._cfg(T.EngineConfig(order="alphabetical"))  # cli.hpp:67-72 unknown ordering
+    c, _ = T._cfg(T.EngineConfig(order=T.OrderKind.by_random(9)))
+    assert (c.order_set, c.order, c.order_seed) == (1, int(T.OrderTag.ByRandom), 9)
+    c, _ = T._cfg(T.EngineConfig(order="coreness"))
+    assert (c.order, c.order_seed) == (int(T.OrderTag.ByCoreness), 0)
+    assert T.EngineConfig().order == T.OrderKind.by_degree()  # engines.hpp:274
     assert T.to_string(T.EngineKind.AnopSurrogate) == "anop-surrogate"
     assert T.to_string(T.CostKind.Dpd) == "DPD"
     plan = T.PartitionPlan(np.array([0, 2, 2, 5, 7], np.uint32))  # test_partition.cpp:97-107
