@@ -119,6 +119,16 @@ tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pa
 tg_status tg_graph_from_csr(int device, uint64_t n, const uint64_t* offsets,
                             const uint32_t* adj, tg_graph** out);
 tg_status tg_graph_free(tg_graph* g);
+/* count_node_iterator_n(effective_adjacency(Graph(n, offsets, adj), by_degree))
+ * in one call from a HOST CSR (graph.hpp:22, effective.hpp:37-52,
+ * sequential.hpp:74-91): the adjacency is streamed to the device in vertex
+ * chunks on a copy stream while the chunks that already arrived are oriented
+ * and every apex whose lists are all resident is counted, so the transfer
+ * hides the orientation and most of the intersection.  Overlap needs
+ * page-locked host buffers (pageable ones work, serialised).  Device
+ * pointers fall back to tg_graph_from_csr + tg_count. */
+tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,
+                            uint64_t* total);
 /* build_graph(parse_edge_list(text), n_override) with both steps on the
  * device (the CLI's --input path, cli.hpp:81-88).  text: len bytes, host or
  * device.  On malformed input: TG_ERR_PARSE, *err_line (may be NULL) = the
@@ -260,6 +270,9 @@ uint64_t tg_kernel_launches(void);
 /* Test hook: shared-memory capacity (entries) of the CTA-path apex staging;
  * lists longer than this are searched in global memory.  0 = default. */
 void tg_debug_set_block_cap(uint32_t entries);
+/* Test hook: adjacency entries per streamed chunk of tg_count_from_csr
+ * (0 = default 2^24; at most 64 chunks). */
+void tg_debug_set_chunk_entries(uint64_t entries);
 /* Test hook: intersection kernels, 0 = automatic (apex groups when the mean
  * oriented list is <= 16 entries, else one apex per warp iteration; 16-byte
  * quad loads when list indices fit 32 bits), 1 = scalar one-apex-per-warp and

@@ -397,6 +397,15 @@ inline VarianceReport variance_report(const Graph& g, const PartitionPlan& plan,
   return {o3[0], o3[1], o3[2], q, v2[0], v2[1]};
 }
 
+/// count_node_iterator_n(effective_adjacency(Graph(n, offsets, adj))) from a
+/// host CSR in one call, the upload overlapped with the count.
+inline std::uint64_t count_from_csr(std::size_t n, const std::uint64_t* offsets, const NodeId* adj,
+                                    int device = 0) {
+  std::uint64_t t = 0;
+  detail::check(tg_count_from_csr(device, n, offsets, adj, &t));
+  return t;
+}
+
 /// io.hpp:24-50 parse_edge_list, on the device.
 inline std::vector<std::pair<NodeId, NodeId>> parse_edge_list(std::string_view text,
                                                               int device = 0) {

@@ -55,6 +55,7 @@ _pvp, _pu64 = C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)
 SIGNATURES = {
     "tg_graph_from_edges": (_i32, [C.c_int, _vp, _u64, _u64, _pvp]),
     "tg_graph_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pvp]),
+    "tg_count_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pu64]),
     "tg_graph_free": (_i32, [_vp]),
     "tg_graph_info": (_i32, [_vp, _pu64, _pu64]),
     "tg_graph_csr": (_i32, [_vp, _vp, _vp]),
@@ -88,6 +89,7 @@ SIGNATURES = {
     "tg_kernel_launches": (_u64, []),
     "tg_last_intersect_ms": (_dbl, [_vp]),
     "tg_debug_set_block_cap": (None, [_u32]),
+    "tg_debug_set_chunk_entries": (None, [_u64]),
     "tg_debug_set_warp_variant": (None, [_i32]),
     "tg_gen_pa": (_i32, [_u64, _u64, _u64, _pvp, _pu64]),
     "tg_gen_gnp": (_i32, [_u64, _dbl, _u64, _pvp, _pu64]),

@@ -17,6 +17,7 @@
 //                follow the request/reply protocol.
 // The multi-process path (one process per GPU, paper_1706_05151_b200/
 // distributed.py) calls the same kernels through the rank-local entries.
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -55,6 +56,7 @@ struct tg_graph {
 namespace {
 
 thread_local std::string t_last_error;
+uint64_t g_chunk_entries = 0;  // tg_count_from_csr chunk size (0: default)
 
 }  // namespace
 void tgb_set_error(const std::string& msg) { t_last_error = msg; }
@@ -491,6 +493,8 @@ uint64_t tg_kernel_launches(void) { return tgb::g_launches; }
 
 void tg_debug_set_block_cap(uint32_t entries) { tgb::g_block_cap = entries; }
 
+void tg_debug_set_chunk_entries(uint64_t entries) { g_chunk_entries = entries; }
+
 void tg_debug_set_warp_variant(int32_t variant) { tgb::g_warp_variant = variant; }
 
 tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pairs,
@@ -588,6 +592,102 @@ tg_status tg_write_edge_list(tg_graph* g, char* out, uint64_t capacity, uint64_t
     return cap_status;
   }
   return st;
+}
+
+tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,
+                            uint64_t* total) {
+  return guard([&] {
+    TG_REQUIRE(total != nullptr && offsets != nullptr, "null argument");
+    TG_REQUIRE(n <= 0xFFFFFFFFull, "n must fit NodeId");
+    if (is_device_ptr(offsets) || (adj && is_device_ptr(adj))) {
+      // already resident: nothing to overlap
+      tg_graph* h = nullptr;
+      tg_status st = tg_graph_from_csr(device, n, offsets, adj, &h);
+      if (st != TG_OK) throw tgb::Error(st, t_last_error);
+      st = tg_count(h, total);
+      const std::string err = t_last_error;
+      tg_graph_free(h);
+      if (st != TG_OK) throw tgb::Error(st, err);
+      return;
+    }
+    const uint64_t m2 = offsets[n];
+    TG_REQUIRE(m2 % 2 == 0, "symmetric CSR must hold an even number of entries");
+    TG_REQUIRE(adj != nullptr || m2 == 0, "null adjacency");
+    tg_graph* g = new_graph(device);
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> evs;
+    auto cleanup = [&] {
+      if (cs) {
+        cudaStreamSynchronize(cs);
+        cudaStreamDestroy(cs);
+      }
+      for (auto e : evs) cudaEventDestroy(e);
+      tg_graph_free(g);
+    };
+    try {
+      cudaStream_t s = g->stream;
+      TG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      g->g.n = n;
+      g->g.m2 = m2;
+      g->g.off.alloc(n + 1, s);
+      g->g.adj.alloc(m2 ? m2 : 1, s);
+      TG_CUDA(cudaStreamSynchronize(s));  // allocations visible to the copy stream
+      // chunks of ~2^24 adjacency entries (64 MB; measured best on C2 among
+      // 2^23..2^27), vertex boundaries on tiles
+      const uint64_t per = g_chunk_entries ? g_chunk_entries : (1ull << 24);
+      const uint64_t K = std::min<uint64_t>(64, std::max<uint64_t>(1, m2 / per));
+      std::vector<uint32_t> cb(K + 1, 0);
+      cb[K] = (uint32_t)n;
+      for (uint64_t k = 1; k < K; ++k) {
+        const uint64_t target = m2 * k / K;
+        const uint64_t v = (uint64_t)(std::lower_bound(offsets, offsets + n + 1, target) - offsets);
+        cb[k] = (uint32_t)std::max<uint64_t>(cb[k - 1], std::min<uint64_t>(n, v & ~31ull));
+      }
+      evs.resize(K + 1);
+      for (auto& e : evs) TG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      auto copy_chunk = [&](uint64_t k) {
+        const uint64_t a = offsets[cb[k]], b = offsets[cb[k + 1]];
+        if (b > a)
+          TG_CUDA(cudaMemcpyAsync(g->g.adj.p + a, adj + a, (b - a) * 4, cudaMemcpyHostToDevice, cs));
+        TG_CUDA(cudaEventRecord(evs[k + 1], cs));
+      };
+      TG_CUDA(cudaMemcpyAsync(g->g.off.p, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, cs));
+      TG_CUDA(cudaEventRecord(evs[0], cs));
+      copy_chunk(0);
+      TG_CUDA(cudaStreamWaitEvent(s, evs[0], 0));
+      tgb::compute_degrees(g->g, s);  // host sync on the offsets only
+      DBuf<uint32_t> bigq, ids(n ? n : 1, s), d_cb(K + 1, s);
+      DBuf<unsigned long long> ctr, cnt(1, s), d_total(1, s);
+      DBuf<uint8_t> ready(n ? n : 1, s);
+      d_total.zero();
+      TG_CUDA(cudaMemcpyAsync(d_cb.p, cb.data(), (K + 1) * 4, cudaMemcpyHostToDevice, s));
+      tgb::orient_chunk_begin(g->g, g->eff, bigq, ctr, s);
+      const CsrView full = view(g->eff);
+      for (uint64_t k = 0; k < K; ++k) {
+        if (k) copy_chunk(k);
+        TG_CUDA(cudaStreamWaitEvent(s, evs[k + 1], 0));
+        tgb::orient_chunk(g->g, g->eff, cb[k], cb[k + 1], bigq.p, ctr.p, s);
+        tgb::ready_chunks(g->eff, d_cb.p, (uint32_t)K, (uint32_t)k, cb[k], cb[k + 1], ready.p, s);
+        tgb::select_ready(ready.p, cb[k + 1], (uint32_t)k, ids.p, cnt.p, s);
+        if (cb[k + 1])
+          tgb::intersect_list(full, ids.p, cnt.p, cb[k + 1], full,
+                              CountOut{d_total.p, nullptr, nullptr, nullptr, 0}, g->scr, s,
+                              g->eff.data.n);
+      }
+      unsigned long long h = 0;
+      download(&h, d_total.p, 1, s);
+      sync(g);
+      *total = h;
+      cudaStream_t keep = cs;
+      cs = nullptr;
+      TG_CUDA(cudaStreamSynchronize(keep));
+      TG_CUDA(cudaStreamDestroy(keep));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
 }
 
 tg_status tg_graph_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,

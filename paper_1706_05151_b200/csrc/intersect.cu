@@ -44,6 +44,21 @@ struct RowsApex {
   }
 };
 
+// apexes given as an id list whose length is known only on the device
+struct ListApex {
+  CsrView view;
+  const uint32_t* ids;
+  const unsigned long long* n;
+  __device__ __forceinline__ uint64_t count() const { return *n; }
+  __device__ __forceinline__ void get(uint64_t k, uint32_t& v, const uint32_t*& L,
+                                      uint32_t& hv) const {
+    v = ids[k];
+    const uint64_t d = view.desc[v - view.base];
+    L = view.data + desc_start(d);
+    hv = desc_len(d);
+  }
+};
+
 struct MsgApex {
   MsgView m;
   __device__ __forceinline__ uint64_t count() const { return m.count; }
@@ -520,6 +535,13 @@ void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32
                     uint64_t nu_entries, bool unrestricted) {
   RowsApex A{apex, vlo, vhi};
   dispatch(A, (uint64_t)(vhi - vlo), nu, ulo, uhi, out, scr, s, !unrestricted, nu_entries);
+}
+
+void intersect_list(CsrView apex, const uint32_t* ids, const unsigned long long* d_count,
+                    uint64_t max_items, CsrView nu, const CountOut& out, IntersectScratch& scr,
+                    cudaStream_t s, uint64_t nu_entries) {
+  ListApex A{apex, ids, d_count};
+  dispatch(A, max_items, nu, 0, 0xffffffffu, out, scr, s, false, nu_entries);
 }
 
 void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,

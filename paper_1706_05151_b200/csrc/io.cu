@@ -1,26 +1,24 @@
 // io.cu -- edge-list text on the device (io.hpp:18-64): parse_edge_list and
 // write_edge_list as HBM-streaming byte kernels.
 //
-// parse (io.hpp:24-50), three passes over the text:
-//   1. k_count_nl   : '\n' count per 64 KB chunk (16-byte loads, popc of a
-//                     byte-compare mask)            -> CUB scan per chunk
-//   2. k_line_ends  : positions of the newlines, ballot-compacted in file order
-//   3. k_parse_lines: one thread per line (consecutive lines in consecutive
-//                     lanes, so a warp reads ~0.5 KB of contiguous text),
-//                     bytes read through an aligned 32-bit window; writes the
-//                     pair (u | v << 32) and a keep flag; a malformed line
-//                     lowers an atomic minimum of the failing line index.
-//   CUB DeviceSelect::Flagged drops blank/comment lines (file order kept).
-// Line i = bytes (end[i-1], end[i]) with end[-1] = -1, so its 1-based line
-// number is i + 1 exactly as the reference counts (io.hpp:30-35).  The
-// ParseError message of the first bad line is formatted on the host from
-// that one line (same rules as the kernel).
+// parse (io.hpp:24-50), two passes of one CTA per 16 KB of text:
+//   1. k_parse_chunks<false>: stage the chunk (+512 B halo) in bank-padded
+//      shared memory; each thread parses the lines starting in its 64-byte
+//      segment with istream semantics; edges per chunk, and an atomic
+//      minimum of the first bad line's byte position;
+//   CUB scan of the chunk counts (file order = chunk order, thread order);
+//   2. k_parse_chunks<true>: the same parse, writing (u | v << 32) at the
+//      chunk offset plus the thread's block prefix.
+// On a bad line its number is 1 + the newlines before it (k_count_nl over the
+// prefix), and the ParseError message is formatted on the host from that one
+// line (same rules as the kernel).
 //
 // write (io.hpp:52-64): a warp per vertex sums the byte lengths of its
 // "u v\n" lines (v > u), CUB scan to row offsets, then lanes write their
 // lines at their warp-scan positions.
 #include <cub/cub.cuh>
 
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -77,89 +75,54 @@ k_count_nl(const uint4* __restrict__ text, uint64_t len, uint64_t* __restrict__ 
   if (threadIdx.x == 0) cnt[c] = t;
 }
 
-// pass 2: newline positions, in file order within each chunk
-__global__ void __launch_bounds__(256)
-k_line_ends(const uint32_t* __restrict__ text, uint64_t len, const uint64_t* __restrict__ base,
-            uint64_t* __restrict__ ends) {
-  const uint64_t c = blockIdx.x;
-  const uint64_t b = c * kChunk, e = min(len, b + kChunk);
-  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __shared__ unsigned s_warp[8];
-  __shared__ uint64_t s_base;
-  if (threadIdx.x == 0) s_base = base[c];
-  __syncthreads();
-  // the block walks the chunk in 1 KB steps (one 4-byte word per thread)
-  for (uint64_t p0 = b; p0 < e; p0 += 1024) {
-    const uint64_t at = p0 + 4 * threadIdx.x;
-    uint32_t m = 0;
-    if (at < e) {
-      m = nl_mask_word(__ldcs(text + at / 4));
-      if (at + 4 > e) m &= (1u << (e - at)) - 1u;
-    }
-    const unsigned k = __popc(m);
-    // block exclusive scan of k in thread order
-    unsigned incl = k;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
-      if ((int)lane >= o) incl += x;
-    }
-    if (lane == 31) s_warp[w] = incl;
-    __syncthreads();
-    unsigned wbase = 0, tot = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      wbase += (i < (int)w) ? s_warp[i] : 0u;
-      tot += s_warp[i];
-    }
-    unsigned pos = wbase + incl - k;
-    const uint64_t ob = s_base;
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      ends[ob + pos++] = at + bit;
-      m &= m - 1;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_base = ob + tot;
-    __syncthreads();
-  }
-}
+// ---- chunk parser: a CTA per 16 KB of text, a thread per 64-byte segment.
+// The chunk (+ a 512-byte halo for lines that cross its end) is staged in
+// shared memory with one pad word per 16 words, so the 32 threads of a warp
+// reading byte k of their own segments (stride 64 B) hit 32 distinct banks.
+// Each thread parses the lines that START in its segment; bytes past the
+// halo (a line longer than 512 B) come from global memory.
+constexpr int kPT = 256;                          // threads per CTA
+constexpr uint32_t kSeg = 64;                     // bytes per thread
+constexpr uint32_t kPChunk = kPT * kSeg;          // 16 KB per CTA
+constexpr uint32_t kHalo = 512;
+constexpr uint32_t kStage = kPChunk + kHalo;      // staged bytes
+constexpr uint32_t kStageWords = kStage / 4 + kStage / 64;  // + 1 pad word / 16
 
-struct ByteWin {
-  const uint32_t* t;
-  uint64_t wi = ~0ull;
-  uint32_t w = 0;
-  __device__ __forceinline__ unsigned at(uint64_t p) {
-    const uint64_t q = p >> 2;
-    if (q != wi) {
-      wi = q;
-      w = __ldg(t + q);
+struct ChunkText {
+  const uint32_t* sw;   // padded shared words
+  const char* g;        // global text
+  uint64_t base, len;   // chunk start, text length
+  uint32_t staged;      // bytes of the chunk staged (from base)
+  __device__ __forceinline__ int at(uint64_t i) const {  // -1 past the text
+    if (i < staged) {
+      const uint32_t w = (uint32_t)(i >> 2);
+      return (sw[w + (w >> 4)] >> (8 * (i & 3))) & 0xff;
     }
-    return (w >> (8 * (p & 3))) & 0xffu;
+    return base + i < len ? (int)(unsigned char)__ldg(g + base + i) : -1;
   }
 };
 
-__device__ __forceinline__ bool is_space(unsigned c) {  // std::isspace, "C" locale
+__device__ __forceinline__ bool is_space(int c) {  // std::isspace, "C" locale
   return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
 }
 
-// istream >> unsigned long long (libstdc++ num_get): skip spaces, sign,
-// digits; overflow fails; '-' negates modulo 2^64
-__device__ __forceinline__ bool extract_ull(ByteWin& bw, uint64_t& i, uint64_t e, uint64_t& out) {
-  unsigned c = 0;
-  while (i < e && is_space(c = bw.at(i))) ++i;
-  if (i >= e) return false;
+// istream >> unsigned long long on one line (libstdc++ num_get): skip
+// spaces, sign, digits; overflow fails; '-' negates modulo 2^64.  The line
+// ends at '\n' or at the end of the text (c < 0).
+__device__ __forceinline__ bool extract_ull(const ChunkText& T, uint64_t& i, uint64_t& out) {
+  int c;
+  while ((c = T.at(i)) >= 0 && c != '\n' && is_space(c)) ++i;
+  if (c < 0 || c == '\n') return false;
   bool neg = false;
   if (c == '+' || c == '-') {
     neg = c == '-';
-    if (++i >= e) return false;
-    c = bw.at(i);
+    c = T.at(++i);
   }
   if (c < '0' || c > '9') return false;
   uint64_t acc = 0;
   bool over = false;
-  while (i < e && (c = bw.at(i)) >= '0' && c <= '9') {
-    const uint64_t d = c - '0';
+  while ((c = T.at(i)) >= '0' && c <= '9') {
+    const uint64_t d = (uint64_t)(c - '0');
     if (acc > (~0ull - d) / 10) over = true;
     else acc = acc * 10 + d;
     ++i;
@@ -169,38 +132,76 @@ __device__ __forceinline__ bool extract_ull(ByteWin& bw, uint64_t& i, uint64_t e
   return true;
 }
 
-// pass 3: one thread per line
-__global__ void __launch_bounds__(256)
-k_parse_lines(const uint32_t* __restrict__ text, uint64_t len, const uint64_t* __restrict__ ends,
-              uint64_t nlines, uint64_t* __restrict__ val, uint8_t* __restrict__ keep,
-              unsigned long long* __restrict__ bad) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nlines;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = i ? ends[i - 1] + 1 : 0;
-    const uint64_t e = ends[i];  // (the last line ends at len)
-    ByteWin bw{text};
-    uint64_t first = b;
-    unsigned c = 0;
-    while (first < e && ((c = bw.at(first)) == ' ' || c == '\t' || c == '\r')) ++first;
-    uint8_t k = 0;
-    uint64_t out = 0;
-    if (first < e && c != '#') {
-      uint64_t p = b, u = 0, v = 0;
-      bool ok = extract_ull(bw, p, e, u) && extract_ull(bw, p, e, v);
-      if (ok) {
-        while (p < e && is_space(bw.at(p))) ++p;
-        ok = p == e;
-      }
-      if (ok) {
-        out = (uint64_t)(uint32_t)u | ((uint64_t)(uint32_t)v << 32);  // static_cast<NodeId>
-        k = 1;
-      } else {
-        atomicMin(bad, (unsigned long long)i);
-      }
-    }
-    val[i] = out;
-    keep[i] = k;
+// io.hpp:37-46 for the line starting at chunk offset p: 0 skip, 1 edge, 2 error
+__device__ __forceinline__ int parse_line(const ChunkText& T, uint64_t p, uint64_t& pair) {
+  int c;
+  uint64_t q = p;
+  while ((c = T.at(q)) == ' ' || c == '\t' || c == '\r') ++q;
+  if (c < 0 || c == '\n' || c == '#') return 0;
+  uint64_t u = 0, v = 0;
+  if (!extract_ull(T, q, u) || !extract_ull(T, q, v)) return 2;
+  while ((c = T.at(q)) >= 0 && c != '\n' && is_space(c)) ++q;
+  if (c >= 0 && c != '\n') return 2;
+  pair = (uint64_t)(uint32_t)u | ((uint64_t)(uint32_t)v << 32);  // static_cast<NodeId>
+  return 1;
+}
+
+// WRITE = false: edges of each thread's segment (tcnt) and the first bad
+// line start (bad); WRITE = true: pairs from the thread's scanned offset.
+template <bool WRITE>
+__global__ void __launch_bounds__(kPT)
+k_parse_chunks(const char* __restrict__ text, uint64_t len, uint32_t* __restrict__ tcnt,
+               const uint64_t* __restrict__ toff, uint64_t* __restrict__ pairs,
+               unsigned long long* __restrict__ bad) {
+  __shared__ uint32_t sw[kStageWords];
+  const uint64_t base = (uint64_t)blockIdx.x * kPChunk;
+  const uint32_t staged = (uint32_t)min((uint64_t)kStage, len - base);
+  const uint4* g4 = reinterpret_cast<const uint4*>(text + base);  // base % 16 == 0
+  for (uint32_t j = threadIdx.x; j * 16 < staged; j += kPT) {
+    const uint4 x = __ldcs(g4 + j);  // the text buffer is padded past len
+    const uint32_t w = 4 * j, pw = w + (w >> 4);
+    sw[pw] = x.x;
+    sw[pw + 1] = x.y;
+    sw[pw + 2] = x.z;
+    sw[pw + 3] = x.w;
   }
+  __syncthreads();
+  const ChunkText T{sw, text, base, len, staged};
+  const uint32_t chunk_len = (uint32_t)min((uint64_t)kPChunk, len - base);
+  const uint32_t sb = threadIdx.x * kSeg, se = min(chunk_len, sb + kSeg);
+  const uint64_t gt = (uint64_t)blockIdx.x * kPT + threadIdx.x;
+  // line starts in the segment: p with byte(p-1) == '\n' (one bit each, from
+  // the staged words), so every thread runs its ~4 line parses back to back
+  // and the warp stays converged (a byte-by-byte walk diverges at every byte)
+  const int prev = sb == 0 ? (base == 0 ? '\n' : (int)(unsigned char)__ldg(text + base - 1))
+                           : (sb < chunk_len ? T.at(sb - 1) : 0);
+  uint64_t starts = 0;
+  if (sb < se) {
+    uint64_t nl = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const uint32_t w = (sb >> 2) + q;
+      nl |= (uint64_t)nl_mask_word(sw[w + (w >> 4)]) << (4 * q);
+    }
+    const uint32_t nb = se - sb;  // <= 64
+    starts = (nl << 1) | (prev == '\n' ? 1ull : 0ull);
+    if (nb < 64) starts &= (1ull << nb) - 1ull;
+  }
+  uint32_t edges = 0;
+  uint64_t out = WRITE ? toff[gt] : 0;
+  while (starts) {
+    const uint32_t p = sb + (uint32_t)(__ffsll((long long)starts) - 1);
+    starts &= starts - 1;
+    uint64_t pr = 0;
+    const int r = parse_line(T, p, pr);
+    if (r == 1) {
+      if (WRITE) pairs[out++] = pr;
+      ++edges;
+    } else if (r == 2 && !WRITE) {
+      atomicMin(bad, (unsigned long long)(base + p));
+    }
+  }
+  if (!WRITE) tcnt[gt] = edges;
 }
 
 // ---- write_edge_list
@@ -240,23 +241,28 @@ k_row_bytes(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj, 
   }
 }
 
+// lines of 32 neighbours are formatted into a per-warp shared buffer, then
+// the warp's contiguous output range is stored as aligned 32-bit words
+constexpr uint32_t kLineMax = 22;  // "4294967295 4294967295\n"
+
+__device__ __forceinline__ void put_digits(char* p, uint32_t x, unsigned d) {
+  for (int k = (int)d - 1; k >= 0; --k) {
+    p[k] = (char)('0' + x % 10);
+    x /= 10;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 k_write_rows(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj, uint64_t n,
              const uint64_t* __restrict__ roff, char* __restrict__ out) {
+  __shared__ __align__(4) char sbuf[8][32 * kLineMax + 4];
   const unsigned lane = threadIdx.x & 31;
+  char* B = sbuf[threadIdx.x >> 5];
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t u = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
     const uint64_t e = off[u + 1];
     const uint64_t s = upper_start(adj, off[u], e, (uint32_t)u);
     const unsigned du = ndigits((uint32_t)u);
-    char ud[10];
-    {
-      uint32_t x = (uint32_t)u;
-      for (int k = (int)du - 1; k >= 0; --k) {
-        ud[k] = (char)('0' + x % 10);
-        x /= 10;
-      }
-    }
     uint64_t base = roff[u];
     for (uint64_t j0 = s; j0 < e; j0 += 32) {
       const uint64_t j = j0 + lane;
@@ -270,21 +276,36 @@ k_write_rows(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
         const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
         if ((int)lane >= o) incl += x;
       }
+      const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
       if (has) {
-        char* p = out + base + incl - l;
-        for (unsigned k = 0; k < du; ++k) p[k] = ud[k];
+        char* p = B + incl - l;
+        put_digits(p, (uint32_t)u, du);
         p[du] = ' ';
-        uint32_t x = v;
-        for (int k = (int)dv - 1; k >= 0; --k) {
-          p[du + 1 + k] = (char)('0' + x % 10);
-          x /= 10;
-        }
+        put_digits(p + du + 1, v, dv);
         p[du + 1 + dv] = '\n';
       }
-      base += __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      // store B[0, tot) at out[base, base + tot): unaligned head, words, tail
+      const unsigned head = min(tot, (unsigned)((4 - (base & 3)) & 3));
+      if (lane < head) out[base + lane] = B[lane];
+      const unsigned nw = (tot - head) >> 2;
+      uint32_t* ow = reinterpret_cast<uint32_t*>(out + base + head);
+      for (unsigned i = lane; i < nw; i += 32) {
+        const char* q = B + head + 4 * i;
+        ow[i] = (uint32_t)(unsigned char)q[0] | ((uint32_t)(unsigned char)q[1] << 8) |
+                ((uint32_t)(unsigned char)q[2] << 16) | ((uint32_t)(unsigned char)q[3] << 24);
+      }
+      const unsigned t0 = head + 4 * nw;
+      if (lane < tot - t0) out[base + t0 + lane] = B[t0 + lane];
+      __syncwarp();
+      base += tot;
     }
   }
 }
+
+struct Widen {
+  __host__ __device__ __forceinline__ uint64_t operator()(uint32_t x) const { return x; }
+};
 
 bool host_space(unsigned char c) {
   return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
@@ -320,67 +341,68 @@ std::string line_error(const std::string& line) {
 uint64_t parse_edge_list_device(const char* d_text, uint64_t len, DBuf<uint32_t>& pairs,
                                 cudaStream_t s, uint64_t* err_line, std::string* err_msg) {
   *err_line = 0;
-  const uint64_t chunks = (len + kChunk - 1) / kChunk;
   if (!len) {
     pairs.alloc(2, s);
     return 0;
   }
-  DBuf<uint64_t> cnt(chunks, s), base(chunks + 1, s);
-  k_count_nl<<<(unsigned)chunks, 256, 0, s>>>((const uint4*)d_text, len, cnt.p);
-  TG_CHECK_LAUNCH();
-  TG_CUDA(cudaMemsetAsync(base.p, 0, 8, s));
-  cub_call(s, [&](void* t, size_t& b) {
-    return cub::DeviceScan::InclusiveSum(t, b, cnt.p, base.p + 1, (int64_t)chunks, s);
-  });
-  uint64_t nl = 0;
-  char last = 0;
-  TG_CUDA(cudaMemcpyAsync(&nl, base.p + chunks, 8, cudaMemcpyDeviceToHost, s));
-  TG_CUDA(cudaMemcpyAsync(&last, d_text + len - 1, 1, cudaMemcpyDeviceToHost, s));
-  TG_CUDA(cudaStreamSynchronize(s));
-  // io.hpp:30-35: a final line without '\n' still counts
-  const uint64_t nlines = nl + (last != '\n' ? 1 : 0);
-  DBuf<uint64_t> ends(nlines ? nlines : 1, s);
-  k_line_ends<<<(unsigned)chunks, 256, 0, s>>>((const uint32_t*)d_text, len, base.p, ends.p);
-  TG_CHECK_LAUNCH();
-  if (nlines > nl) TG_CUDA(cudaMemcpyAsync(ends.p + nl, &len, 8, cudaMemcpyHostToDevice, s));
-  DBuf<uint64_t> val(nlines ? nlines : 1, s);
-  DBuf<uint8_t> keep(nlines ? nlines : 1, s);
+  const uint64_t chunks = (len + kPChunk - 1) / kPChunk;
+  TG_REQUIRE(chunks < (1ull << 31), "text too large");
+  const uint64_t nt = chunks * kPT;  // one count per 64-byte segment
+  DBuf<uint32_t> tcnt(nt, s);
+  DBuf<uint64_t> toff(nt + 1, s);
   DBuf<unsigned long long> bad(1, s);
   TG_CUDA(cudaMemsetAsync(bad.p, 0xff, 8, s));
-  if (nlines) {
-    k_parse_lines<<<grid_for(nlines, 256, 148u * 16u), 256, 0, s>>>(
-        (const uint32_t*)d_text, len, ends.p, nlines, val.p, keep.p, bad.p);
-    TG_CHECK_LAUNCH();
-  }
-  g_launches += 5;
+  k_parse_chunks<false><<<(unsigned)chunks, kPT, 0, s>>>(d_text, len, tcnt.p, nullptr, nullptr, bad.p);
+  TG_CHECK_LAUNCH();
+  TG_CUDA(cudaMemsetAsync(toff.p, 0, 8, s));
+  // 64-bit accumulation (a text may hold more than 2^32 lines)
+  cub::TransformInputIterator<uint64_t, Widen, const uint32_t*> wide(tcnt.p, Widen());
+  cub_call(s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::InclusiveSum(t, b, wide, toff.p + 1, (int64_t)nt, s);
+  });
+  uint64_t E = 0;
   unsigned long long h_bad = 0;
+  TG_CUDA(cudaMemcpyAsync(&E, toff.p + nt, 8, cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaMemcpyAsync(&h_bad, bad.p, 8, cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
+  g_launches += 3;
   if (h_bad != ~0ull) {
-    uint64_t be[2] = {0, 0};
-    if (h_bad) TG_CUDA(cudaMemcpyAsync(&be[0], ends.p + h_bad - 1, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaMemcpyAsync(&be[1], ends.p + h_bad, 8, cudaMemcpyDeviceToHost, s));
-    TG_CUDA(cudaStreamSynchronize(s));
-    const uint64_t b = h_bad ? be[0] + 1 : 0;
-    std::string line(be[1] - b, '\0');
-    if (!line.empty())
-      TG_CUDA(cudaMemcpy(&line[0], d_text + b, line.size(), cudaMemcpyDeviceToHost));
-    *err_line = h_bad + 1;
-    *err_msg = "line " + std::to_string(h_bad + 1) + ": " + line_error(line);
+    // line number: 1 + newlines in [0, bad); the line: [bad, next '\n')
+    uint64_t nl = 0;
+    if (h_bad) {
+      const uint64_t nc = (h_bad + kChunk - 1) / kChunk;
+      DBuf<uint64_t> c2(nc, s), tot(1, s);
+      k_count_nl<<<(unsigned)nc, 256, 0, s>>>((const uint4*)d_text, h_bad, c2.p);
+      TG_CHECK_LAUNCH();
+      cub_call(s, [&](void* t, size_t& b) {
+        return cub::DeviceReduce::Sum(t, b, c2.p, tot.p, (int64_t)nc, s);
+      });
+      TG_CUDA(cudaMemcpyAsync(&nl, tot.p, 8, cudaMemcpyDeviceToHost, s));
+      TG_CUDA(cudaStreamSynchronize(s));
+      g_launches += 2;
+    }
+    std::string line;
+    for (uint64_t p = h_bad; p < len;) {  // the bad line, 4 KB at a time
+      char buf[4096];
+      const uint64_t k = std::min<uint64_t>(sizeof(buf), len - p);
+      TG_CUDA(cudaMemcpy(buf, d_text + p, k, cudaMemcpyDeviceToHost));
+      const char* e = static_cast<const char*>(memchr(buf, '\n', k));
+      line.append(buf, e ? (size_t)(e - buf) : k);
+      if (e) break;
+      p += k;
+    }
+    *err_line = nl + 1;
+    *err_msg = "line " + std::to_string(nl + 1) + ": " + line_error(line);
     return 0;
   }
-  // drop blank / comment lines, keeping file order
-  pairs.alloc(2 * (nlines ? nlines : 1), s);
-  DBuf<int64_t> nsel(1, s);
-  cub_call(s, [&](void* t, size_t& b) {
-    return cub::DeviceSelect::Flagged(t, b, val.p, keep.p, (uint64_t*)pairs.p, nsel.p,
-                                      (int64_t)nlines, s);
-  });
-  ++g_launches;
-  int64_t E = 0;
-  TG_CUDA(cudaMemcpyAsync(&E, nsel.p, 8, cudaMemcpyDeviceToHost, s));
-  TG_CUDA(cudaStreamSynchronize(s));
-  return (uint64_t)E;
+  pairs.alloc(2 * (E ? E : 1), s);
+  if (E) {
+    k_parse_chunks<true><<<(unsigned)chunks, kPT, 0, s>>>(d_text, len, nullptr, toff.p,
+                                                          (uint64_t*)pairs.p, nullptr);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
+  }
+  return E;
 }
 
 uint64_t write_edge_list_device(const DevGraph& g, DBuf<char>& out, cudaStream_t s) {

@@ -254,7 +254,8 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
                uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff,
                unsigned long long* __restrict__ tile_ctr, uint32_t* __restrict__ bigq,
                unsigned long long* __restrict__ bigq_n, uint32_t* __restrict__ kmask,
-               const uint64_t* __restrict__ hcnt) {
+               const uint64_t* __restrict__ hcnt, uint64_t tile_lo = 0,
+               uint64_t tile_hi = ~0ull) {
   __shared__ uint32_t sTbl[kOWarps][kOTbl + kOUnroll];
   __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
   __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
@@ -263,10 +264,10 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
   uint32_t* Tbl = sTbl[w];
-  const uint64_t ntiles = (n + 31) / 32;
+  const uint64_t ntiles = min((n + 31) / 32, tile_hi);  // tiles [tile_lo, ntiles)
   for (;;) {
     unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(tile_ctr, 1ull);
+    if (lane == 0) t = tile_lo + atomicAdd(tile_ctr, 1ull);
     t = __shfl_sync(FULL, t, 0);
     if (t >= ntiles) break;
     const uint64_t v0 = t * 32;
@@ -889,6 +890,123 @@ static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
                                                ctr.p, g.m2, out.desc.p, out.data.p);
   TG_CHECK_LAUNCH();
   g_launches += 2;
+}
+
+// ---- chunked one-pass orientation (host CSR streamed in vertex chunks) ----
+//
+// The tile layout is position-independent (each tile writes inside its own
+// adjacency range; hubs reserve slots above m2 with one atomic), so tiles can
+// be oriented in any grouping: orient_chunk orients the tiles of vertices
+// [vb, ve) (multiples of 32 except at n) as soon as their adjacency arrived.
+// c[6] counters persist across chunks: [0] tile claims (reset per chunk),
+// [1] medium-big queue size, [2] hub-region slots, [3] hubs, [4]/[5] hub /
+// medium claim cursors (restarted at the previous chunk's queue ends).
+__global__ void k_chunk_prep(unsigned long long* c) {
+  c[0] = 0;
+  c[4] = c[3];
+  c[5] = c[1];
+}
+
+__device__ __forceinline__ uint32_t chunk_of(const uint32_t* __restrict__ cb, uint32_t K, uint32_t u) {
+  uint32_t lo = 0, hi = K;  // first chunk whose end exceeds u
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (cb[mid + 1] <= u) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ready chunk of each apex of chunk k: its lists and every N_u it intersects
+// with are oriented once chunk max(k, chunk(max N_v)) is (lists ID-sorted);
+// apexes with h_v < 2 close no triangle (0xff)
+__global__ void k_ready_chunk(const uint64_t* __restrict__ edesc, const uint32_t* __restrict__ eff,
+                              const uint32_t* __restrict__ cb, uint32_t K, uint32_t k, uint32_t vb,
+                              uint32_t ve, uint8_t* __restrict__ ready) {
+  for (uint64_t v = vb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < ve;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = edesc[v];
+    const uint32_t h = desc_len(d);
+    uint8_t r = 0xff;
+    if (h >= 2) r = (uint8_t)max(k, chunk_of(cb, K, eff[desc_start(d) + h - 1]));
+    ready[v] = r;
+  }
+}
+
+// apexes v < ve whose ready chunk is k (any order)
+__global__ void k_select_ready(const uint8_t* __restrict__ ready, uint32_t ve, uint32_t k,
+                               uint32_t* __restrict__ ids, unsigned long long* __restrict__ cnt) {
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < ve;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = base + lane;
+    const bool take = v < ve && ready[v] == k;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (!bal) continue;
+    unsigned long long at = 0;
+    if (lane == 0) at = atomicAdd(cnt, (unsigned long long)__popc(bal));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (take) ids[at + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)v;
+  }
+}
+
+void orient_chunk_begin(const DevGraph& g, DevEff& out, DBuf<uint32_t>& bigq,
+                        DBuf<unsigned long long>& ctr, cudaStream_t s) {
+  TG_REQUIRE(g.m2 + g.big_entries + kQuadPad < (1ull << 34), "graph too large for chunked orientation");
+  out.rows = g.n;
+  out.base = 0;
+  out.compact = false;
+  out.entries = g.m2 / 2;
+  if (out.desc.n < (g.n ? g.n : 1)) out.desc.alloc(g.n ? g.n : 1, s);
+  if (out.data.n < g.m2 + g.big_entries + kQuadPad) out.data.alloc(g.m2 + g.big_entries + kQuadPad, s);
+  out.off.release();
+  bigq.alloc(g.n ? g.n : 1, s);
+  ctr.alloc(6, s);
+  ctr.zero();
+}
+
+void orient_chunk(const DevGraph& g, DevEff& out, uint32_t vb, uint32_t ve, uint32_t* bigq,
+                  unsigned long long* ctr, cudaStream_t s) {
+  if (ve <= vb) return;
+  const uint64_t t_lo = vb / 32, t_hi = ((uint64_t)ve + 31) / 32;
+  const unsigned grid = grid_for(t_hi - t_lo, kOWarps, 148u * kOBlocks);
+  k_chunk_prep<<<1, 1, 0, s>>>(ctr);
+  TG_CHECK_LAUNCH();
+  const bool coded = order_coded(g);
+  if (coded)
+    k_orient_tiles<2, true><<<grid, kOWarps * 32, 0, s>>>(
+        g.off.p, g.adj.p, order_key(g), g.dcode.p, g.n, nullptr, out.desc.p, out.data.p, ctr,
+        bigq, ctr + 1, nullptr, nullptr, t_lo, t_hi);
+  else
+    k_orient_tiles<2, false><<<grid, kOWarps * 32, 0, s>>>(
+        g.off.p, g.adj.p, order_key(g), g.dcode.p, g.n, nullptr, out.desc.p, out.data.p, ctr,
+        bigq, ctr + 1, nullptr, nullptr, t_lo, t_hi);
+  TG_CHECK_LAUNCH();
+  if (coded)
+    k_orient_big1<true><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq, g.n,
+                                                ctr, g.m2, out.desc.p, out.data.p);
+  else
+    k_orient_big1<false><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq,
+                                                 g.n, ctr, g.m2, out.desc.p, out.data.p);
+  TG_CHECK_LAUNCH();
+  g_launches += 3;
+}
+
+void ready_chunks(const DevEff& e, const uint32_t* d_cb, uint32_t K, uint32_t k, uint32_t vb,
+                  uint32_t ve, uint8_t* ready, cudaStream_t s) {
+  if (ve <= vb) return;
+  k_ready_chunk<<<grid_for(ve - vb, 256), 256, 0, s>>>(e.desc.p, e.data.p, d_cb, K, k, vb, ve, ready);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
+void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
+                  unsigned long long* cnt, cudaStream_t s) {
+  TG_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+  if (!ve) return;
+  k_select_ready<<<grid_for(ve, 256), 256, 0, s>>>(ready, ve, k, ids, cnt);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
 }
 
 // effective.hpp:37-52 for the whole graph (the hot path), no host sync.

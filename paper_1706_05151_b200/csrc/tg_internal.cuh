@@ -164,6 +164,20 @@ void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cud
 // Orient the whole graph (no host sync): one-pass tile layout, or compact.
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s);
 void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s);
+// Chunked one-pass orientation (tile layout) for a CSR that arrives in
+// vertex chunks: begin sizes `out` and the queue/counters; orient_chunk
+// orients vertices [vb, ve) (vb a multiple of 32); ready_chunks records for
+// each apex of chunk k the chunk after which it can be counted (chunk vertex
+// boundaries d_cb, K+1 entries, device); select_ready lists the apexes
+// v < ve whose ready chunk is k into ids, their number into *cnt (device).
+void orient_chunk_begin(const DevGraph& g, DevEff& out, DBuf<uint32_t>& bigq,
+                        DBuf<unsigned long long>& ctr, cudaStream_t s);
+void orient_chunk(const DevGraph& g, DevEff& out, uint32_t vb, uint32_t ve, uint32_t* bigq,
+                  unsigned long long* ctr, cudaStream_t s);
+void ready_chunks(const DevEff& e, const uint32_t* d_cb, uint32_t K, uint32_t k, uint32_t vb,
+                  uint32_t ve, uint8_t* ready, cudaStream_t s);
+void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
+                  unsigned long long* cnt, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
 // sum of list lengths over rows [lo, hi) (host result).
@@ -228,6 +242,11 @@ struct IntersectScratch {
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
                     uint32_t uhi, const CountOut& out, IntersectScratch& scr,
                     cudaStream_t s, uint64_t nu_entries, bool unrestricted);
+// NodeIteratorN over an apex LIST (ids, *d_count entries, device; at most
+// max_items): the pipelined count's ready apexes.
+void intersect_list(CsrView apex, const uint32_t* ids, const unsigned long long* d_count,
+                    uint64_t max_items, CsrView nu, const CountOut& out, IntersectScratch& scr,
+                    cudaStream_t s, uint64_t nu_entries);
 // SurrogateCount (engines.hpp:60-76) over received messages.
 void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
                     const CountOut& out, IntersectScratch& scr, cudaStream_t s,

@@ -146,6 +146,26 @@ def build_graph(edge_pairs, n_override: int = 0, device: int = 0) -> Graph:
     return Graph(h, device)
 
 
+def count_from_csr(n: int, offsets, adj, device: int = 0) -> int:
+    """count_node_iterator_n(effective_adjacency(Graph(n, offsets, adj))) in
+    one call from a host CSR (graph.hpp:22, sequential.hpp:74-91): the
+    upload is streamed in vertex chunks and overlapped with orientation and
+    counting (pass page-locked buffers, e.g. ``torch.Tensor.pin_memory()``
+    views, for the overlap).  ``offsets``/``adj``: numpy arrays or objects
+    with ``data_ptr()``."""
+    def ptr(a, dt):
+        if hasattr(a, "data_ptr"):
+            return C.c_void_p(a.data_ptr()), a
+        a = np.ascontiguousarray(a, dtype=dt)
+        return (_p(a) if a.size else None), a
+    po, ko = ptr(offsets, np.uint64)
+    pa, ka = ptr(adj, np.uint32)
+    t = C.c_uint64()
+    check(lib().tg_count_from_csr(device, int(n), po, pa, C.byref(t)))
+    del ko, ka
+    return t.value
+
+
 def build_graph_from_pointer(ptr: int, num_pairs: int, n_override: int = 0,
                              device: int = 0) -> Graph:
     """build_graph from a raw (host or device) pointer to interleaved pairs."""

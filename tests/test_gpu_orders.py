@@ -182,3 +182,26 @@ def test_node_iterator_pp_all_orders(orders_golden):
                 k = kind(o["order"], o["seed"])
                 assert T.count_node_iterator_pp(g, k) == o["count"], (name, k)
                 assert T.count_node_iterator_pp(g, k, use_intersection=True) == o["count"]
+
+
+@pytest.mark.parametrize("chunk", [0, 64, 1000, 4096])
+def test_count_from_csr_streamed(chunk):
+    """tg_count_from_csr: the streamed host-CSR count (chunked orientation,
+    apexes counted once all their lists arrived) equals the oracle for any
+    chunking, including chunks smaller than one hub's adjacency."""
+    import torch
+
+    L = lib()
+    try:
+        L.tg_debug_set_chunk_entries(chunk)
+        for pairs, n_over in ((T.gen_pa(20000, 20, 3), 0), (T.gen_rmat(12, 8, 0.57, 0.19, 0.19, 5), 0),
+                              (T.gen_ws(5000, 10, 0.2, 1), 5003),
+                              (np.zeros((0, 2), np.uint32), 7)):
+            ref = O.build_graph(pairs, n_over)
+            want = O.count(ref)[0]
+            assert T.count_from_csr(ref.n, ref.off, ref.adj) == want
+            off_p = torch.from_numpy(ref.off.view(np.int64)).pin_memory()
+            adj_p = torch.from_numpy(ref.adj.view(np.int32)).pin_memory()
+            assert T.count_from_csr(ref.n, off_p, adj_p) == want
+    finally:
+        L.tg_debug_set_chunk_entries(0)
