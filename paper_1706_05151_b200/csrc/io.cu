@@ -102,6 +102,24 @@ struct ChunkText {
   }
 };
 
+// sequential reader over one line: one shared-memory word per 4 bytes
+struct Cursor {
+  const ChunkText& T;
+  uint64_t i;
+  uint32_t wi = 0xffffffffu, w = 0;
+  __device__ __forceinline__ int peek() {
+    if (i < T.staged) {
+      const uint32_t q = (uint32_t)(i >> 2);
+      if (q != wi) {
+        wi = q;
+        w = T.sw[q + (q >> 4)];
+      }
+      return (w >> (8 * (i & 3))) & 0xff;
+    }
+    return T.at(i);
+  }
+};
+
 __device__ __forceinline__ bool is_space(int c) {  // std::isspace, "C" locale
   return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
 }
@@ -109,23 +127,24 @@ __device__ __forceinline__ bool is_space(int c) {  // std::isspace, "C" locale
 // istream >> unsigned long long on one line (libstdc++ num_get): skip
 // spaces, sign, digits; overflow fails; '-' negates modulo 2^64.  The line
 // ends at '\n' or at the end of the text (c < 0).
-__device__ __forceinline__ bool extract_ull(const ChunkText& T, uint64_t& i, uint64_t& out) {
+__device__ __forceinline__ bool extract_ull(Cursor& R, uint64_t& out) {
   int c;
-  while ((c = T.at(i)) >= 0 && c != '\n' && is_space(c)) ++i;
+  while ((c = R.peek()) >= 0 && c != '\n' && is_space(c)) ++R.i;
   if (c < 0 || c == '\n') return false;
   bool neg = false;
   if (c == '+' || c == '-') {
     neg = c == '-';
-    c = T.at(++i);
+    ++R.i;
+    c = R.peek();
   }
   if (c < '0' || c > '9') return false;
   uint64_t acc = 0;
   bool over = false;
-  while ((c = T.at(i)) >= '0' && c <= '9') {
-    const uint64_t d = (uint64_t)(c - '0');
-    if (acc > (~0ull - d) / 10) over = true;
-    else acc = acc * 10 + d;
-    ++i;
+  while ((c = R.peek()) >= '0' && c <= '9') {
+    const uint64_t lo = acc * 10, sum = lo + (uint64_t)(c - '0');
+    over |= (__umul64hi(acc, 10) != 0) | (sum < lo);  // acc * 10 + d >= 2^64
+    acc = sum;
+    ++R.i;
   }
   if (over) return false;
   out = neg ? 0ull - acc : acc;
@@ -134,13 +153,13 @@ __device__ __forceinline__ bool extract_ull(const ChunkText& T, uint64_t& i, uin
 
 // io.hpp:37-46 for the line starting at chunk offset p: 0 skip, 1 edge, 2 error
 __device__ __forceinline__ int parse_line(const ChunkText& T, uint64_t p, uint64_t& pair) {
+  Cursor R{T, p};
   int c;
-  uint64_t q = p;
-  while ((c = T.at(q)) == ' ' || c == '\t' || c == '\r') ++q;
+  while ((c = R.peek()) == ' ' || c == '\t' || c == '\r') ++R.i;
   if (c < 0 || c == '\n' || c == '#') return 0;
   uint64_t u = 0, v = 0;
-  if (!extract_ull(T, q, u) || !extract_ull(T, q, v)) return 2;
-  while ((c = T.at(q)) >= 0 && c != '\n' && is_space(c)) ++q;
+  if (!extract_ull(R, u) || !extract_ull(R, v)) return 2;
+  while ((c = R.peek()) >= 0 && c != '\n' && is_space(c)) ++R.i;
   if (c >= 0 && c != '\n') return 2;
   pair = (uint64_t)(uint32_t)u | ((uint64_t)(uint32_t)v << 32);  // static_cast<NodeId>
   return 1;

@@ -99,8 +99,11 @@ inline const uint32_t* order_key(const DevGraph& g) {
   return g.order == TG_ORDER_BY_DEGREE ? g.deg.p : g.okey.p;
 }
 // 1-byte degree codes once the 4-byte degrees would not stay in L2.
+#ifndef TG_CODED_MIN_N
+#define TG_CODED_MIN_N (32ull << 20)
+#endif
 inline bool order_coded(const DevGraph& g) {
-  return g.order == TG_ORDER_BY_DEGREE && g.n > (32ull << 20);
+  return g.order == TG_ORDER_BY_DEGREE && g.n > (uint64_t)(TG_CODED_MIN_N);
 }
 
 // Monotone 1-byte code of a degree: exact below 240, then one bucket per
