@@ -277,8 +277,14 @@ void tg_debug_set_chunk_entries(uint64_t entries);
  * oriented list is <= 16 entries, else one apex per warp iteration; 16-byte
  * quad loads when list indices fit 32 bits), 1 = scalar one-apex-per-warp and
  * scalar CTA path, 2 = quad apex groups, 3 = quad one-apex-per-warp, 4 =
- * scalar apex groups.  All exact. */
+ * scalar apex groups, 5 = lane-per-edge groups (lane.cuh).  All exact. */
 void tg_debug_set_warp_variant(int32_t variant);
+/* Test hook: the large-graph code paths on small graphs.  orient_mode: 0
+ * auto, 1 compact count/scan/fill orientation (taken above 2^34 list
+ * slots), +4 = 1-byte degree codes as orientation keys (taken above 32M
+ * vertices); force_wide: 64-bit element indices in the scalar
+ * intersection kernels (taken above 2^32 list slots).  All exact. */
+void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide);
 /* Device-side time (ms) of the last intersection pass (CUDA events on the
  * launching stream); 0 if none. */
 double tg_last_intersect_ms(tg_graph* g);

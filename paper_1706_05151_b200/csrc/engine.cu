@@ -497,6 +497,11 @@ void tg_debug_set_chunk_entries(uint64_t entries) { g_chunk_entries = entries; }
 
 void tg_debug_set_warp_variant(int32_t variant) { tgb::g_warp_variant = variant; }
 
+void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide) {
+  tgb::g_orient_mode = orient_mode;
+  tgb::g_force_wide = force_wide != 0;
+}
+
 tg_status tg_graph_from_edges(int device, const uint32_t* pairs, uint64_t num_pairs,
                               uint64_t n_override, tg_graph** out) {
   return guard([&] {

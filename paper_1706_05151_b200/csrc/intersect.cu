@@ -399,6 +399,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "quad.cuh"
 #include "ctaq.cuh"
 #include "groupq.cuh"
+#include "lane.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
@@ -412,6 +413,17 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // tail; measured: scalar groups win on Watts-Strogatz (mean list 10), quad
   // groups on R-MAT (15.5), quad per-apex on PA (20).
   const int wv = g_warp_variant;
+  if (wv == 5) {  // lane-per-edge groups (lane.cuh)
+    const unsigned ggrid = grid_for(items, kLWarps * 32, 148u * 6u);
+    uint64_t chunk = items / ((uint64_t)ggrid * kLWarps * 8);
+    chunk = chunk < 32 ? 32 : (chunk > 256 ? 256 : chunk);
+    k_intersect_lane<TALLY, LIST, FILTER, Apex><<<ggrid, kLWarps * 32, 0, s>>>(
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+        (uint32_t)chunk);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
+    return;
+  }
   const bool groups = wv == 0 ? nu.avg_len <= 16.f : (wv == 2 || wv == 4);
   const bool quads = nu.quad_ok && (wv == 0 ? (!groups || nu.avg_len >= 14.f) : (wv == 2 || wv == 3));
   if (!groups && quads) {  // one apex per warp iteration, quad loads
@@ -500,7 +512,7 @@ void dispatch(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t 
               const CountOut& out, IntersectScratch& scr, cudaStream_t s, bool filter,
               uint64_t data_entries) {
   const bool tally = out.tally != nullptr, list = out.tri != nullptr;
-  const bool wide = data_entries >= (1ull << 32);
+  const bool wide = data_entries >= (1ull << 32) || g_force_wide;
   nu.quad_ok = data_entries < (1ull << 34);  // quad indices fit 32 bits
   if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
   else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
@@ -524,6 +536,7 @@ __global__ void k_cc(const uint64_t* __restrict__ off, uint64_t n,
 
 uint32_t g_block_cap = 0;
 int g_warp_variant = 0;
+bool g_force_wide = false;
 
 void IntersectScratch::ensure(uint64_t cap, cudaStream_t s) {
   if (big.n < cap) big.alloc(cap, s);

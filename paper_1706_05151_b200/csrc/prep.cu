@@ -27,6 +27,7 @@
 namespace tgb {
 
 unsigned long long g_launches = 0;
+int g_orient_mode = 0;
 
 namespace {
 
@@ -1019,7 +1020,8 @@ void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
   const uint64_t slots = g.m2 + g.big_entries;
-  if (!g.n || slots + kQuadPad >= (1ull << 34)) return orient_full_compact(g, out, s);
+  if (!g.n || slots + kQuadPad >= (1ull << 34) || (g_orient_mode & 3) == 1)
+    return orient_full_compact(g, out, s);
   out.rows = g.n;
   out.base = 0;
   out.compact = false;

@@ -94,6 +94,8 @@ struct DevGraph {
   DBuf<uint32_t> okey;     // n (non-degree orders only)
 };
 
+extern int g_orient_mode;  // (see below)
+
 // Order key array and key kind used by the orientation kernels.
 inline const uint32_t* order_key(const DevGraph& g) {
   return g.order == TG_ORDER_BY_DEGREE ? g.deg.p : g.okey.p;
@@ -103,7 +105,8 @@ inline const uint32_t* order_key(const DevGraph& g) {
 #define TG_CODED_MIN_N (32ull << 20)
 #endif
 inline bool order_coded(const DevGraph& g) {
-  return g.order == TG_ORDER_BY_DEGREE && g.n > (uint64_t)(TG_CODED_MIN_N);
+  return g.order == TG_ORDER_BY_DEGREE &&
+         (g.n > (uint64_t)(TG_CODED_MIN_N) || (g_orient_mode & 4));
 }
 
 // Monotone 1-byte code of a degree: exact below 240, then one bucket per
@@ -284,6 +287,11 @@ extern unsigned long long g_launches;
 extern uint32_t g_block_cap;
 // warp-path kernel: 0 = automatic, 1 = one apex per warp iteration, 2 = groups
 extern int g_warp_variant;
+// tests: 64-bit element indexing in the scalar kernels on small graphs (the
+// > 2^32-slot path), and the orientation layout (0 auto, 1 compact
+// count/scan/fill, 2 one-pass tiles; +4 = 1-byte degree codes)
+extern bool g_force_wide;
+extern int g_orient_mode;
 
 inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap = 148u * 64u) {
   uint64_t g = (work + block - 1) / block;
