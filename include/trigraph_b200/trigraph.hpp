@@ -16,6 +16,7 @@
 #define TRIGRAPH_B200_TRIGRAPH_HPP
 
 #include <array>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <map>
@@ -438,6 +439,20 @@ inline std::string write_edge_list(const Graph& g) {
   std::string out(len, '\0');
   if (len) detail::check(tg_write_edge_list(g.handle(), &out[0], len, &len));
   return out;
+}
+
+/// stats.hpp:21-23 (host arithmetic, as in the reference).
+inline double normalized_triangle_count(std::uint64_t triangles, std::size_t n) {
+  return n == 0 ? 0.0 : static_cast<double>(triangles) / static_cast<double>(n);
+}
+
+/// stats.hpp:11-19 (host arithmetic, as in the reference).
+inline std::uint64_t estimate_p_opt(double n, double dbar, double base_n, double base_dbar,
+                                    double base_p_opt) {
+  if (n <= 0 || dbar <= 0 || base_n <= 0 || base_dbar <= 0 || base_p_opt <= 0)
+    throw std::invalid_argument("estimate_p_opt: all inputs must be positive");
+  const double est = base_p_opt * (dbar / base_dbar) * std::sqrt(n / base_n);
+  return static_cast<std::uint64_t>(std::llround(est));
 }
 
 /// io.hpp:129-162 gen_pa (host, bit-identical edge stream).

@@ -602,6 +602,22 @@ def variance_report(g: Graph, plan: PartitionPlan, q: float) -> VarianceReport:
 # ---------------------------------------------------------------- generators
 
 
+def normalized_triangle_count(triangles: int, n: int) -> float:
+    """stats.hpp:21-23: mean triangles per node."""
+    return 0.0 if n == 0 else float(triangles) / float(n)
+
+
+def estimate_p_opt(n: float, dbar: float, base_n: float, base_dbar: float,
+                   base_p_opt: float) -> int:
+    """stats.hpp:11-19: p_opt extrapolated linearly in average degree and in
+    sqrt(n) from a calibrated base network (llround, as std::llround)."""
+    import math
+    if n <= 0 or dbar <= 0 or base_n <= 0 or base_dbar <= 0 or base_p_opt <= 0:
+        raise ValueError("estimate_p_opt: all inputs must be positive")
+    est = base_p_opt * (dbar / base_dbar) * math.sqrt(n / base_n)
+    return int(math.floor(est + 0.5)) if est >= 0 else int(math.ceil(est - 0.5))
+
+
 def _pairs_from(fn, *args) -> np.ndarray:
     ptr = C.c_void_p()
     cnt = C.c_uint64()

@@ -85,3 +85,13 @@ def test_no_cpu_fallback_without_gpu():
         pass
     with pytest.raises((_lib.TrigraphError, ValueError)):
         T.build_graph([(0, 1), (1, 2), (0, 2)])
+
+
+def test_stats_helpers():
+    # stats.hpp:11-23; acceptance.cpp:469-476 (p_opt extrapolation: 120 * sqrt(25) = 600)
+    assert T.estimate_p_opt(25e6, 50, 1e6, 50, 120) == 600
+    assert T.estimate_p_opt(1e6, 100, 1e6, 50, 3) == 6
+    with pytest.raises(ValueError):
+        T.estimate_p_opt(0, 50, 1e6, 50, 120)
+    assert T.normalized_triangle_count(10, 4) == 2.5
+    assert T.normalized_triangle_count(10, 0) == 0.0
