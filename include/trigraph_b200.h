@@ -279,6 +279,11 @@ void tg_debug_set_chunk_entries(uint64_t entries);
  * scalar CTA path, 2 = quad apex groups, 3 = quad one-apex-per-warp, 4 =
  * scalar apex groups, 5 = lane-per-edge groups (lane.cuh).  All exact. */
 void tg_debug_set_warp_variant(int32_t variant);
+/* Test hook: the bitmap CTA path (apexes whose rank window, n - rank(v) - 1,
+ * fits cap_bits of shared memory; ctab.cuh).  mode 0 = automatic (on when
+ * lists longer than 64 hold > 1% of the oriented entries), 1 = on, 2 = off;
+ * cap_bits 0 = 2^19.  All exact. */
+void tg_debug_set_rank_bitmap(int32_t mode, uint32_t cap_bits);
 /* Test hook: the large-graph code paths on small graphs.  orient_mode: 0
  * auto, 1 compact count/scan/fill orientation (taken above 2^34 list
  * slots), +4 = 1-byte degree codes as orientation keys (taken above 32M

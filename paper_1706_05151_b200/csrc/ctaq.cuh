@@ -23,7 +23,8 @@ template <bool TALLY, bool LIST, bool FILTER, class Apex>
 __global__ void __launch_bounds__(kCT, 2)
 k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                  const uint32_t* __restrict__ big, const unsigned long long* __restrict__ big_count,
-                 uint64_t big_cap, uint32_t tcap_log2, unsigned long long* __restrict__ work_ctr) {
+                 uint64_t big_cap, uint32_t tcap_log2, unsigned long long* __restrict__ work_ctr,
+                 RankView skip) {
   using Scan = cub::BlockScan<uint32_t, kCT>;
   extern __shared__ __align__(16) uint32_t sHt[];  // hash table (2^tcap_log2 slots) + filter
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -58,6 +59,11 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
     uint32_t v, hv;
     const uint32_t* L;
     A.get(big[bi], v, L, hv);
+    // apexes whose rank window fits the bitmap path ran on k_intersect_ctab
+    if (skip.rank && skip.n - (skip.rank[v] + 1u) <= skip.cap_bits) {
+      __syncthreads();  // sItem is rewritten at the loop top
+      continue;
+    }
     uint32_t bits = 3;
     while ((1u << bits) < hv) ++bits;
     bool in_ht = (4u << bits) <= tcap;

@@ -31,6 +31,12 @@ struct tg_graph {
   tgb::DevGraph g;
   bool have_eff = false;
   tgb::DevEff eff;
+  uint64_t eff_gen = 0;          // bumped by every (re)orientation
+  // bitmap CTA path (ctab.cuh): order rank + rank-labelled lists
+  int rank_mode = -1;            // -1 undecided, 0 off, 1 on (per order)
+  bool have_rk = false;
+  uint64_t rdata_gen = ~0ull;    // rdata matches eff iff rdata_gen == eff_gen
+  tgb::DBuf<uint32_t> rk, rdata;
   tgb::IntersectScratch scr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
@@ -46,7 +52,7 @@ struct tg_graph {
   template <class F>
   void for_each_buf(F&& f) {
     f(g.off); f(g.adj); f(g.deg); f(g.dcode); f(g.okey);
-    f(eff.off); f(eff.data); f(eff.desc);
+    f(eff.off); f(eff.data); f(eff.desc); f(rk); f(rdata);
     f(scr.big); f(scr.big_count);
     f(part.off); f(part.data); f(part.desc);
     f(pack.desc); f(pack.doff);
@@ -57,6 +63,8 @@ namespace {
 
 thread_local std::string t_last_error;
 uint64_t g_chunk_entries = 0;  // tg_count_from_csr chunk size (0: default)
+int g_rank_bitmap = 0;         // bitmap CTA path: 0 auto, 1 on, 2 off
+uint32_t g_rank_cap = 0;       // its window capacity in bits (0: 2^19)
 
 }  // namespace
 void tgb_set_error(const std::string& msg) { t_last_error = msg; }
@@ -81,6 +89,7 @@ tg_status guard(F&& f) {
 
 using tgb::CountOut;
 using tgb::CsrView;
+using tgb::RankView;
 using tgb::DBuf;
 using tgb::DevEff;
 
@@ -146,13 +155,43 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
   tgb::set_order(g->g, kind, sd, g->stream);
   g->have_eff = false;
   g->have_part = false;
+  g->have_rk = false;
+  g->rank_mode = -1;
+}
+
+// (Re)orient the whole graph (effective.hpp:37-52).
+void orient(tg_graph* g) {
+  tgb::orient_full(g->g, g->eff, g->stream);
+  g->have_eff = true;
+  ++g->eff_gen;
 }
 
 void ensure_eff(tg_graph* g) {
-  if (!g->have_eff) {
-    tgb::orient_full(g->g, g->eff, g->stream);
-    g->have_eff = true;
+  if (!g->have_eff) orient(g);
+}
+
+// The bitmap CTA path's inputs when it pays (auto: the apexes with > 64
+// oriented entries -- the CTA path -- hold more than 1% of the entries), or
+// as forced by tg_debug_set_rank_bitmap.  Rebuilds the rank-labelled lists
+// after every orientation (a gather over the m entries).
+RankView rank_view(tg_graph* g) {
+  const uint64_t n = g->g.n;
+  if (g_rank_bitmap == 2 || !n || g->eff.data.n + tgb::kQuadPad >= (1ull << 34)) return {};
+  cudaStream_t s = g->stream;
+  if (g_rank_bitmap == 0 && g->rank_mode < 0)
+    g->rank_mode = tgb::heavy_entries(g->eff, 64, s) * 100 > g->eff.entries ? 1 : 0;
+  if (g_rank_bitmap == 0 && g->rank_mode == 0) return {};
+  if (!g->have_rk) {
+    g->rk.alloc(n, s);
+    tgb::order_rank(g->g, g->rk.p, s);
+    g->have_rk = true;
   }
+  if (g->rdata_gen != g->eff_gen) {
+    if (g->rdata.n < g->eff.data.n) g->rdata.alloc(g->eff.data.n, s);
+    tgb::rank_lists(g->eff, g->rk.p, g->rdata.p, s);
+    g->rdata_gen = g->eff_gen;
+  }
+  return RankView{g->rk.p, g->rdata.p, (uint32_t)n, g_rank_cap ? g_rank_cap : (1u << 19)};
 }
 
 // Counting pass with CUDA-event timing of the intersection kernels.
@@ -238,7 +277,9 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
                               nullptr, 0, s);
     const DevEff& E = sp ? es : g->eff;
     const CsrView ev = view(E);
-    timed_pass(g, [&] { tgb::intersect_rows(ev, 0, N, ev, 0, N, out_for(0), g->scr, s, E.data.n, true);
+    timed_pass(g, [&] {
+      const RankView rv = sp ? RankView{} : rank_view(g);
+      tgb::intersect_rows(ev, 0, N, ev, 0, N, out_for(0), g->scr, s, E.data.n, true, rv);
     });
     R.per_rank[0].stored_entries = g->eff.entries;
   } else if (sp && cfg.engine == TG_ENGINE_AOP) {
@@ -264,10 +305,11 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
     const DevEff& E = sp ? es : g->eff;
     const CsrView ev = view(E);
     timed_pass(g, [&] {
+      const RankView rv = sp ? RankView{} : rank_view(g);
       for (uint64_t i = 0; i < p; ++i)
         if (b[i + 1] > b[i])
           tgb::intersect_rows(ev, b[i], b[i + 1], ev, 0, N, out_for(i), g->scr, s,
-                              E.data.n, true);
+                              E.data.n, true, rv);
     });
     if (cfg.engine == TG_ENGINE_AOP) {
       for (uint64_t i = 0; i < p; ++i)
@@ -372,7 +414,7 @@ uint64_t seq_count(tg_graph* g) {
   const uint32_t N = (uint32_t)g->g.n;
   timed_pass(g, [&] {
     tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                        g->eff.data.n, true);
+                        g->eff.data.n, true, rank_view(g));
   });
   unsigned long long h = 0;
   download(&h, ctr.p, 1, s);
@@ -408,7 +450,7 @@ void list_in_pieces(tg_graph* g, uint32_t lo, uint32_t hi, DBuf<uint32_t>& tri, 
   DBuf<unsigned long long> c(2, s);
   c.zero();
   tgb::intersect_rows(full, lo, hi, full, 0, N, CountOut{c.p, nullptr, nullptr, nullptr, 0},
-                      g->scr, s, g->eff.data.n, true);
+                      g->scr, s, g->eff.data.n, true, rank_view(g));
   unsigned long long cnt = 0;
   download(&cnt, c.p, 1, s);
   sync(g);
@@ -496,6 +538,11 @@ void tg_debug_set_block_cap(uint32_t entries) { tgb::g_block_cap = entries; }
 void tg_debug_set_chunk_entries(uint64_t entries) { g_chunk_entries = entries; }
 
 void tg_debug_set_warp_variant(int32_t variant) { tgb::g_warp_variant = variant; }
+
+void tg_debug_set_rank_bitmap(int32_t mode, uint32_t cap_bits) {
+  g_rank_bitmap = mode;
+  g_rank_cap = cap_bits ? std::max<uint32_t>(32, (cap_bits + 31) & ~31u) : 0;
+}
 
 void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide) {
   tgb::g_orient_mode = orient_mode;
@@ -1041,15 +1088,14 @@ tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
     TG_REQUIRE(d_total != nullptr, "null output");
     cudaStream_t s = g->stream;
     // orientation: effective_adjacency (effective.hpp:37-52), rebuilt
-    tgb::orient_full(g->g, g->eff, s);
-    g->have_eff = true;
+    orient(g);
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
     const CsrView full = view(g->eff);
     const uint32_t N = (uint32_t)g->g.n;
     timed_pass(g, [&] {
       tgb::intersect_rows(full, 0, N, full, 0, N,
                           CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                          g->eff.data.n, true);
+                          g->eff.data.n, true, rank_view(g));
     });
   });
 }
@@ -1057,8 +1103,7 @@ tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
 tg_status tg_orient_device(tg_graph* g) {
   return guard([&] {
     enter(g);
-    tgb::orient_full(g->g, g->eff, g->stream);
-    g->have_eff = true;
+    orient(g);
   });
 }
 
@@ -1074,7 +1119,7 @@ tg_status tg_count_device(tg_graph* g, uint64_t* d_total) {
     timed_pass(g, [&] {
       tgb::intersect_rows(full, 0, N, full, 0, N,
                           CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                          g->eff.data.n, true);
+                          g->eff.data.n, true, rank_view(g));
     });
   });
 }
@@ -1103,7 +1148,7 @@ tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p
       if (ce > cb)
         tgb::intersect_rows(full, cb, ce, full, 0, N,
                             CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                          g->eff.data.n, true);
+                          g->eff.data.n, true, rank_view(g));
     });
   });
 }

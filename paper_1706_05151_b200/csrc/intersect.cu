@@ -400,6 +400,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "ctaq.cuh"
 #include "groupq.cuh"
 #include "lane.cuh"
+#include "ctab.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
@@ -461,7 +462,7 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
 // factor 1/4; g_block_cap (tests) lowers it to exercise the global fallback.
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
 void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const CountOut& out,
-                IntersectScratch& scr, cudaStream_t s) {
+                IntersectScratch& scr, cudaStream_t s, const RankView& rv) {
   uint32_t tl2 = 14;
   if (g_block_cap) {
     tl2 = 5;
@@ -469,10 +470,19 @@ void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const Cou
   }
   const int dyn = (int)((1u << tl2) * 4 + (1u << tl2) / 2);  // table + filter (tcap/8 words)
   if (nu.quad_ok && g_warp_variant != 1) {  // quad loads
+    if (rv.rank) {  // apexes whose rank window fits a bitmap (ctab.cuh) first
+      const int bdyn = (int)(rv.cap_bits / 8);
+      TG_CUDA(cudaFuncSetAttribute(k_intersect_ctab<TALLY, LIST, FILTER, Apex>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bdyn));
+      k_intersect_ctab<TALLY, LIST, FILTER, Apex><<<148 * 2, kCT, bdyn, s>>>(
+          A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, rv, scr.big_count.p + 3);
+      TG_CHECK_LAUNCH();
+      ++g_launches;
+    }
     TG_CUDA(cudaFuncSetAttribute(k_intersect_ctaq<TALLY, LIST, FILTER, Apex>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     k_intersect_ctaq<TALLY, LIST, FILTER, Apex><<<148 * 2, kCT, dyn, s>>>(
-        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, tl2, scr.big_count.p + 1);
+        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, tl2, scr.big_count.p + 1, rv);
   } else {
     TG_CUDA(cudaFuncSetAttribute(k_intersect_cta<TALLY, LIST, FILTER, WIDE, Apex>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
@@ -486,11 +496,12 @@ void launch_cta(const Apex& A, CsrView nu, uint32_t ulo, uint32_t uhi, const Cou
 template <bool TALLY, bool LIST, class Apex>
 void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
                  const CountOut& out, IntersectScratch& scr, cudaStream_t s, bool filter,
-                 bool wide) {
+                 bool wide, const RankView& rv) {
   if (!items) return;
   scr.ensure(items, s);
-  // [0]: long-apex queue size, [1]: CTA work counter, [2]: warp-path chunk counter
-  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, 3 * sizeof(unsigned long long), s));
+  // [0]: long-apex queue size, [1]: CTA work counter, [2]: warp-path chunk
+  // counter, [3]: bitmap-CTA work counter
+  TG_CUDA(cudaMemsetAsync(scr.big_count.p, 0, 4 * sizeof(unsigned long long), s));
   if (filter) {
     if (wide) launch_warp<TALLY, LIST, true, true>(A, items, nu, ulo, uhi, out, scr, s);
     else launch_warp<TALLY, LIST, true, false>(A, items, nu, ulo, uhi, out, scr, s);
@@ -499,25 +510,39 @@ void launch_pair(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
     else launch_warp<TALLY, LIST, false, false>(A, items, nu, ulo, uhi, out, scr, s);
   }
   if (filter) {
-    if (wide) launch_cta<TALLY, LIST, true, true>(A, nu, ulo, uhi, out, scr, s);
-    else launch_cta<TALLY, LIST, true, false>(A, nu, ulo, uhi, out, scr, s);
+    if (wide) launch_cta<TALLY, LIST, true, true>(A, nu, ulo, uhi, out, scr, s, rv);
+    else launch_cta<TALLY, LIST, true, false>(A, nu, ulo, uhi, out, scr, s, rv);
   } else {
-    if (wide) launch_cta<TALLY, LIST, false, true>(A, nu, ulo, uhi, out, scr, s);
-    else launch_cta<TALLY, LIST, false, false>(A, nu, ulo, uhi, out, scr, s);
+    if (wide) launch_cta<TALLY, LIST, false, true>(A, nu, ulo, uhi, out, scr, s, rv);
+    else launch_cta<TALLY, LIST, false, false>(A, nu, ulo, uhi, out, scr, s, rv);
   }
 }
 
 template <class Apex>
 void dispatch(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32_t uhi,
               const CountOut& out, IntersectScratch& scr, cudaStream_t s, bool filter,
-              uint64_t data_entries) {
+              uint64_t data_entries, const RankView& rv = RankView{}) {
   const bool tally = out.tally != nullptr, list = out.tri != nullptr;
   const bool wide = data_entries >= (1ull << 32) || g_force_wide;
   nu.quad_ok = data_entries < (1ull << 34);  // quad indices fit 32 bits
-  if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
-  else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
-  else if (list) launch_pair<false, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
-  else launch_pair<false, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide);
+  if (tally && list) launch_pair<true, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide, rv);
+  else if (tally) launch_pair<true, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide, rv);
+  else if (list) launch_pair<false, true>(A, items, nu, ulo, uhi, out, scr, s, filter, wide, rv);
+  else launch_pair<false, false>(A, items, nu, ulo, uhi, out, scr, s, filter, wide, rv);
+}
+
+// rdata[slot] = rank[data[slot]] over every list (a warp per vertex)
+__global__ void k_rank_lists(const uint64_t* __restrict__ desc, const uint32_t* __restrict__ data,
+                             uint64_t rows, const uint32_t* __restrict__ rank,
+                             uint32_t* __restrict__ rdata) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < rows; v += warps) {
+    const uint64_t d = desc[v];
+    const uint64_t b = desc_start(d);
+    const uint32_t h = desc_len(d);
+    for (uint32_t i = lane; i < h; i += 32) rdata[b + i] = __ldg(rank + __ldg(data + b + i));
+  }
 }
 
 __global__ void k_cc(const uint64_t* __restrict__ off, uint64_t n,
@@ -540,21 +565,32 @@ bool g_force_wide = false;
 
 void IntersectScratch::ensure(uint64_t cap, cudaStream_t s) {
   if (big.n < cap) big.alloc(cap, s);
-  if (big_count.n < 3) big_count.alloc(3, s);
+  if (big_count.n < 4) big_count.alloc(4, s);
+}
+
+void rank_lists(const DevEff& e, const uint32_t* d_rank, uint32_t* rdata, cudaStream_t s) {
+  if (!e.rows) return;
+  k_rank_lists<<<grid_for(e.rows * 32, 256, 148u * 32u), 256, 0, s>>>(e.desc.p, e.data.p, e.rows,
+                                                                    d_rank, rdata);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
 }
 
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
                     uint32_t uhi, const CountOut& out, IntersectScratch& scr, cudaStream_t s,
-                    uint64_t nu_entries, bool unrestricted) {
+                    uint64_t nu_entries, bool unrestricted, const RankView& rv) {
   RowsApex A{apex, vlo, vhi};
-  dispatch(A, (uint64_t)(vhi - vlo), nu, ulo, uhi, out, scr, s, !unrestricted, nu_entries);
+  // the bitmap path reads N_v's rank labels at N_v's slots: apex lists must be nu's
+  const RankView r = apex.data == nu.data && apex.desc == nu.desc ? rv : RankView{};
+  dispatch(A, (uint64_t)(vhi - vlo), nu, ulo, uhi, out, scr, s, !unrestricted, nu_entries, r);
 }
 
 void intersect_list(CsrView apex, const uint32_t* ids, const unsigned long long* d_count,
                     uint64_t max_items, CsrView nu, const CountOut& out, IntersectScratch& scr,
-                    cudaStream_t s, uint64_t nu_entries) {
+                    cudaStream_t s, uint64_t nu_entries, const RankView& rv) {
   ListApex A{apex, ids, d_count};
-  dispatch(A, max_items, nu, 0, 0xffffffffu, out, scr, s, false, nu_entries);
+  const RankView r = apex.data == nu.data && apex.desc == nu.desc ? rv : RankView{};
+  dispatch(A, max_items, nu, 0, 0xffffffffu, out, scr, s, false, nu_entries, r);
 }
 
 void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,

@@ -1098,6 +1098,32 @@ void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s) {
   g_launches += 5;
 }
 
+__global__ void k_heavy_lens(const uint64_t* __restrict__ desc, uint64_t rows, uint32_t thr,
+                             unsigned long long* __restrict__ acc) {
+  uint64_t s = 0;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = desc_len(desc[r]);
+    if (h > thr) s += h;
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(acc, (unsigned long long)s);
+}
+
+uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s) {
+  DBuf<unsigned long long> acc(1, s);
+  acc.zero();
+  if (e.rows) {
+    k_heavy_lens<<<grid_for(e.rows, 256, 148u * 8u), 256, 0, s>>>(e.desc.p, e.rows, thr, acc.p);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
+  }
+  unsigned long long h = 0;
+  TG_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
 uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s) {
   DBuf<unsigned long long> acc(1, s);
   acc.zero();

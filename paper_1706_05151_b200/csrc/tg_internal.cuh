@@ -186,6 +186,8 @@ void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
                   unsigned long long* cnt, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
+// sum of the lengths of the lists longer than thr (host result).
+uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s);
 // sum of list lengths over rows [lo, hi) (host result).
 uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s);
 void degree_rank(const DevGraph& g, uint32_t* d_rank, cudaStream_t s);
@@ -227,6 +229,16 @@ struct CountOut {
   uint64_t cap;
 };
 
+// Rank-labelled view for the bitmap CTA path (ctab.cuh): rank[v] = position
+// of v in the orientation order, rdata = the oriented lists with every id
+// replaced by its rank (same slots as the id data).  rank == nullptr: off.
+struct RankView {
+  const uint32_t* rank = nullptr;
+  const uint32_t* rdata = nullptr;
+  uint32_t n = 0;
+  uint32_t cap_bits = 0;  // bitmap capacity (window of ranks above an apex)
+};
+
 // Apexes: either CSR rows [vlo, vhi) of `apex` or packed surrogate messages.
 struct MsgView {
   const uint32_t* hdr;   // 2*count: (v, len)
@@ -247,12 +259,16 @@ struct IntersectScratch {
 // `unrestricted` = [ulo, uhi) covers every vertex (no middle-vertex filter).
 void intersect_rows(CsrView apex, uint32_t vlo, uint32_t vhi, CsrView nu, uint32_t ulo,
                     uint32_t uhi, const CountOut& out, IntersectScratch& scr,
-                    cudaStream_t s, uint64_t nu_entries, bool unrestricted);
+                    cudaStream_t s, uint64_t nu_entries, bool unrestricted,
+                    const RankView& rv = RankView{});
 // NodeIteratorN over an apex LIST (ids, *d_count entries, device; at most
 // max_items): the pipelined count's ready apexes.
 void intersect_list(CsrView apex, const uint32_t* ids, const unsigned long long* d_count,
                     uint64_t max_items, CsrView nu, const CountOut& out, IntersectScratch& scr,
-                    cudaStream_t s, uint64_t nu_entries);
+                    cudaStream_t s, uint64_t nu_entries, const RankView& rv = RankView{});
+// Rank-labelled copy of the oriented lists of `e` (all rows): rdata[slot] =
+// rank[data[slot]] for every list slot (rdata sized like e.data).
+void rank_lists(const DevEff& e, const uint32_t* d_rank, uint32_t* rdata, cudaStream_t s);
 // SurrogateCount (engines.hpp:60-76) over received messages.
 void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
                     const CountOut& out, IntersectScratch& scr, cudaStream_t s,

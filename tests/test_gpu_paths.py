@@ -58,3 +58,35 @@ def test_forced_large_graph_paths(graph, orient_mode, force_wide, variant):
     finally:
         L.tg_debug_set_paths(0, 0)
         L.tg_debug_set_warp_variant(0)
+
+
+@pytest.mark.parametrize("graph", sorted(GRAPHS))
+@pytest.mark.parametrize("cap", [0, 1024, 65536])
+@pytest.mark.parametrize("order", ["degree", "id", "coreness"])
+def test_rank_bitmap_cta_path(graph, cap, order):
+    """The bitmap CTA path (ctab.cuh), forced on with several window
+    capacities so apexes split between it and the hash CTA path: counts,
+    tallies, listings, AOP per-rank counts and per-edge counts exact."""
+    pairs = GRAPHS[graph]()
+    ref = O.build_graph(pairs)
+    want_T, want_tv, want_tri = O.count(ref, tally=True, listing=True, order=order)
+    want_aop = O.run_engine(ref, "aop", 3, order=order)
+    L = lib()
+    kinds = {"degree": T.OrderKind.by_degree(), "id": T.OrderKind.by_id(),
+             "coreness": T.OrderKind.by_coreness()}
+    try:
+        L.tg_debug_set_rank_bitmap(1, cap)
+        with T.build_graph(pairs) as g:
+            cfg = T.EngineConfig(engine=T.EngineKind.Sequential, order=kinds[order],
+                                 track_nodes=True, collect_triangles=True)
+            r = T.run_engine(g, cfg)
+            assert r.total == want_T
+            assert np.array_equal(r.node_counts, want_tv)
+            assert np.array_equal(sorted_triples(r.triangles_list), want_tri)
+            a = T.run_engine(g, T.EngineConfig(engine=T.EngineKind.Aop, ranks=3, order=kinds[order]))
+            assert [x.triangles for x in a.per_rank] == want_aop.triangles.tolist()
+            if order == "degree":
+                assert np.array_equal(T.per_edge_triangle_counts(g), O.per_edge_counts(ref))
+                assert T.count_node_iterator_n(g) == want_T
+    finally:
+        L.tg_debug_set_rank_bitmap(0, 0)

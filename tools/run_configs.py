@@ -51,6 +51,9 @@ def main():
     L = lib()
     if os.environ.get("TG_WARP_VARIANT"):
         L.tg_debug_set_warp_variant(int(os.environ["TG_WARP_VARIANT"]))
+    if os.environ.get("TG_RANK_BITMAP") or os.environ.get("TG_RANK_CAP"):
+        L.tg_debug_set_rank_bitmap(int(os.environ.get("TG_RANK_BITMAP", "0")),
+                                   int(os.environ.get("TG_RANK_CAP", "0")))
     for name in a.configs:
         kind, p = CONFIGS[name]
         p = dict(p)
