@@ -34,6 +34,7 @@ struct tg_graph {
   uint64_t eff_gen = 0;          // bumped by every (re)orientation
   // bitmap CTA path (ctab.cuh): order rank + rank-labelled lists
   int rank_mode = -1;            // -1 undecided, 0 off, 1 on (per order)
+  int near_mode = -1;            // locality warp path (near.cuh): -1 undecided
   bool have_rk = false;
   uint64_t rdata_gen = ~0ull;    // rdata matches eff iff rdata_gen == eff_gen
   tgb::DBuf<uint32_t> rk, rdata;
@@ -157,6 +158,7 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
   g->have_part = false;
   g->have_rk = false;
   g->rank_mode = -1;
+  g->near_mode = -1;
 }
 
 // (Re)orient the whole graph (effective.hpp:37-52).
@@ -168,6 +170,20 @@ void orient(tg_graph* g) {
 
 void ensure_eff(tg_graph* g) {
   if (!g->have_eff) orient(g);
+}
+
+// The full oriented CSR as a kernel view, with the locality flag of the
+// near.cuh warp path: >= 1/2 of the oriented entries lie within 32 ids of
+// their row (decided once per orientation order; one reduction + sync).
+CsrView full_view(tg_graph* g) {
+  ensure_eff(g);
+  if (g->near_mode < 0) {
+    const uint64_t m = g->eff.entries;
+    g->near_mode = m && tgb::near_entries(g->eff, g->stream) * 2 >= m ? 1 : 0;
+  }
+  CsrView v = view(g->eff);
+  v.near_ok = g->near_mode == 1;
+  return v;
 }
 
 // The bitmap CTA path's inputs when it pays (auto: the apexes with > 64
@@ -257,7 +273,7 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
   auto out_for = [&](uint64_t i) {
     return CountOut{ctr.p + i, d_tally, d_tri, d_cursor, cap};
   };
-  const CsrView full = view(g->eff);
+  const CsrView full = full_view(g);
   const uint32_t N = (uint32_t)n;
   // sparsify.hpp: the engines below count over sparsified lists; partition
   // storage (stored_entries) is reported as built, before sparsification
@@ -276,7 +292,7 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
     if (sp) tgb::sparsify_eff(g->eff, es, sq, sseed, sp == TG_SPARSIFY_PER_PARTITION ? 1 : 0,
                               nullptr, 0, s);
     const DevEff& E = sp ? es : g->eff;
-    const CsrView ev = view(E);
+    const CsrView ev = sp ? view(E) : full_view(g);
     timed_pass(g, [&] {
       const RankView rv = sp ? RankView{} : rank_view(g);
       tgb::intersect_rows(ev, 0, N, ev, 0, N, out_for(0), g->scr, s, E.data.n, true, rv);
@@ -303,7 +319,7 @@ EngineResult run(tg_graph* g, const tg_config& cfg, unsigned long long* d_tally,
     if (sp) tgb::sparsify_eff(g->eff, es, sq, sseed, 0,
                               sp == TG_SPARSIFY_PER_PARTITION ? d_b.p : nullptr, p, s);
     const DevEff& E = sp ? es : g->eff;
-    const CsrView ev = view(E);
+    const CsrView ev = sp ? view(E) : full_view(g);
     timed_pass(g, [&] {
       const RankView rv = sp ? RankView{} : rank_view(g);
       for (uint64_t i = 0; i < p; ++i)
@@ -410,7 +426,7 @@ uint64_t seq_count(tg_graph* g) {
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> ctr(1, s);
   ctr.zero();
-  const CsrView full = view(g->eff);
+  const CsrView full = full_view(g);
   const uint32_t N = (uint32_t)g->g.n;
   timed_pass(g, [&] {
     tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, g->scr, s,
@@ -445,7 +461,7 @@ void list_in_pieces(tg_graph* g, uint32_t lo, uint32_t hi, DBuf<uint32_t>& tri, 
                     F&& f) {
   if (hi <= lo) return;
   cudaStream_t s = g->stream;
-  const CsrView full = view(g->eff);
+  const CsrView full = full_view(g);
   const uint32_t N = (uint32_t)g->g.n;
   DBuf<unsigned long long> c(2, s);
   c.zero();
@@ -714,7 +730,7 @@ tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, con
       d_total.zero();
       TG_CUDA(cudaMemcpyAsync(d_cb.p, cb.data(), (K + 1) * 4, cudaMemcpyHostToDevice, s));
       tgb::orient_chunk_begin(g->g, g->eff, bigq, ctr, s);
-      const CsrView full = view(g->eff);
+      const CsrView full = view(g->eff);  // (the locality path stays off here)
       for (uint64_t k = 0; k < K; ++k) {
         if (k) copy_chunk(k);
         TG_CUDA(cudaStreamWaitEvent(s, evs[k + 1], 0));
@@ -1090,7 +1106,7 @@ tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
     // orientation: effective_adjacency (effective.hpp:37-52), rebuilt
     orient(g);
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
-    const CsrView full = view(g->eff);
+    const CsrView full = full_view(g);
     const uint32_t N = (uint32_t)g->g.n;
     timed_pass(g, [&] {
       tgb::intersect_rows(full, 0, N, full, 0, N,
@@ -1114,7 +1130,7 @@ tg_status tg_count_device(tg_graph* g, uint64_t* d_total) {
     cudaStream_t s = g->stream;
     ensure_eff(g);
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
-    const CsrView full = view(g->eff);
+    const CsrView full = full_view(g);
     const uint32_t N = (uint32_t)g->g.n;
     timed_pass(g, [&] {
       tgb::intersect_rows(full, 0, N, full, 0, N,
@@ -1141,7 +1157,7 @@ tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p
     TG_REQUIRE(boundaries[0] == 0 && boundaries[p] <= g->g.n, "invalid boundaries");
     ensure_eff(g);
     cudaStream_t s = g->stream;
-    const CsrView full = view(g->eff);
+    const CsrView full = full_view(g);
     const uint32_t N = (uint32_t)g->g.n;
     const uint32_t cb = boundaries[rank], ce = boundaries[rank + 1];
     timed_pass(g, [&] {

@@ -73,7 +73,7 @@ def test_orders_against_golden(orders_golden, which):
                     assert sha(sorted_triples(r.triangles_list)) == rec_e["triangles_sha256"]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 def test_long_lists_under_id_order(variant):
     """ById orients every edge toward the larger id, so PA's oldest vertices
     carry lists of thousands of entries (the CTA path, and with a lowered
