@@ -120,8 +120,8 @@ struct Cursor {
   }
 };
 
-__device__ __forceinline__ bool is_space(int c) {  // std::isspace, "C" locale
-  return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+__device__ __forceinline__ bool is_space(int c) {  // std::isspace, "C" locale: \t \n \v \f \r ' '
+  return (unsigned)c <= 32u && ((0x100003E00ull >> c) & 1ull);
 }
 
 // istream >> unsigned long long on one line (libstdc++ num_get): skip
@@ -138,14 +138,25 @@ __device__ __forceinline__ bool extract_ull(Cursor& R, uint64_t& out) {
     c = R.peek();
   }
   if (c < '0' || c > '9') return false;
+  // the first 9 digits accumulate in 32 bits (no overflow possible); the
+  // 64-bit multiply with the overflow test only runs for longer numbers
+  uint32_t a32 = 0, nd = 0;
   uint64_t acc = 0;
   bool over = false;
   while ((c = R.peek()) >= '0' && c <= '9') {
-    const uint64_t lo = acc * 10, sum = lo + (uint64_t)(c - '0');
-    over |= (__umul64hi(acc, 10) != 0) | (sum < lo);  // acc * 10 + d >= 2^64
-    acc = sum;
+    const uint32_t d = (uint32_t)(c - '0');
+    if (nd < 9) {
+      a32 = a32 * 10u + d;
+    } else {
+      if (nd == 9) acc = a32;
+      const uint64_t lo = acc * 10, sum = lo + d;
+      over |= (__umul64hi(acc, 10) != 0) | (sum < lo);  // acc * 10 + d >= 2^64
+      acc = sum;
+    }
+    ++nd;
     ++R.i;
   }
+  if (nd <= 9) acc = a32;
   if (over) return false;
   out = neg ? 0ull - acc : acc;
   return true;
