@@ -277,9 +277,8 @@ void tg_debug_set_chunk_entries(uint64_t entries);
  * oriented list is <= 16 entries, else one apex per warp iteration; 16-byte
  * quad loads when list indices fit 32 bits), 1 = scalar one-apex-per-warp and
  * scalar CTA path, 2 = quad apex groups, 3 = quad one-apex-per-warp, 4 =
- * scalar apex groups, 5 = lane-per-edge groups (lane.cuh), 6 = locality groups
- * (near.cuh, automatic when most oriented entries lie within 32 ids of their
- * row).  All exact. */
+ * scalar apex groups, 5 = lane-per-edge groups (lane.cuh), 6 = scalar groups
+ * with id-window membership masks (groupn.cuh).  All exact. */
 void tg_debug_set_warp_variant(int32_t variant);
 /* Test hook: the bitmap CTA path (apexes whose rank window, n - rank(v) - 1,
  * fits cap_bits of shared memory; ctab.cuh).  mode 0 = automatic (on when

@@ -34,7 +34,6 @@ struct tg_graph {
   uint64_t eff_gen = 0;          // bumped by every (re)orientation
   // bitmap CTA path (ctab.cuh): order rank + rank-labelled lists
   int rank_mode = -1;            // -1 undecided, 0 off, 1 on (per order)
-  int near_mode = -1;            // locality warp path (near.cuh): -1 undecided
   bool have_rk = false;
   uint64_t rdata_gen = ~0ull;    // rdata matches eff iff rdata_gen == eff_gen
   tgb::DBuf<uint32_t> rk, rdata;
@@ -158,7 +157,6 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
   g->have_part = false;
   g->have_rk = false;
   g->rank_mode = -1;
-  g->near_mode = -1;
 }
 
 // (Re)orient the whole graph (effective.hpp:37-52).
@@ -172,18 +170,10 @@ void ensure_eff(tg_graph* g) {
   if (!g->have_eff) orient(g);
 }
 
-// The full oriented CSR as a kernel view, with the locality flag of the
-// near.cuh warp path: >= 1/2 of the oriented entries lie within 32 ids of
-// their row (decided once per orientation order; one reduction + sync).
+// The full oriented CSR as a kernel view (oriented on first use).
 CsrView full_view(tg_graph* g) {
   ensure_eff(g);
-  if (g->near_mode < 0) {
-    const uint64_t m = g->eff.entries;
-    g->near_mode = m && tgb::near_entries(g->eff, g->stream) * 2 >= m ? 1 : 0;
-  }
-  CsrView v = view(g->eff);
-  v.near_ok = g->near_mode == 1;
-  return v;
+  return view(g->eff);
 }
 
 // The bitmap CTA path's inputs when it pays (auto: the apexes with > 64

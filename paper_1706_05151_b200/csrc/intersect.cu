@@ -400,7 +400,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "ctaq.cuh"
 #include "groupq.cuh"
 #include "lane.cuh"
-#include "near.cuh"
+#include "groupn.cuh"
 #include "ctab.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
@@ -415,11 +415,11 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // tail; measured: scalar groups win on Watts-Strogatz (mean list 10), quad
   // groups on R-MAT (15.5), quad per-apex on PA (20).
   const int wv = g_warp_variant;
-  if (wv == 6) {  // near.cuh (measured slower than the group kernel on C4)
-    const unsigned ggrid = grid_for(items, kLWarps * 32, 148u * 6u);
-    uint64_t chunk = items / ((uint64_t)ggrid * kLWarps * 8);
+  if (wv == 6) {  // groupn.cuh (measured slower than group.cuh on C4)
+    const unsigned ggrid = grid_for(items, kGWarps * 32, 148u * 5u);
+    uint64_t chunk = items / ((uint64_t)ggrid * kGWarps * 8);
     chunk = chunk < 32 ? 32 : (chunk > 256 ? 256 : chunk);
-    k_intersect_near<TALLY, LIST, FILTER, Apex><<<ggrid, kLWarps * 32, 0, s>>>(
+    k_intersect_groupn<TALLY, LIST, FILTER, WIDE, Apex><<<ggrid, kGWarps * 32, 0, s>>>(
         A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
         (uint32_t)chunk);
     TG_CHECK_LAUNCH();

@@ -1110,36 +1110,6 @@ __global__ void k_heavy_lens(const uint64_t* __restrict__ desc, uint64_t rows, u
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(acc, (unsigned long long)s);
 }
 
-__global__ void k_near_entries(const uint64_t* __restrict__ desc, const uint32_t* __restrict__ data,
-                               uint64_t rows, uint32_t base, unsigned long long* __restrict__ acc) {
-  const unsigned lane = threadIdx.x & 31;
-  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  uint64_t c = 0;
-  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
-    const uint64_t d = desc[r];
-    const uint64_t b = desc_start(d);
-    const uint32_t h = desc_len(d), v = base + (uint32_t)r;
-    for (uint32_t i = lane; i < h; i += 32) c += (data[b + i] - v + 32u) < 64u;
-  }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0 && c) atomicAdd(acc, (unsigned long long)c);
-}
-
-uint64_t near_entries(const DevEff& e, cudaStream_t s) {
-  DBuf<unsigned long long> acc(1, s);
-  acc.zero();
-  if (e.rows) {
-    k_near_entries<<<grid_for(e.rows * 32, 256, 148u * 32u), 256, 0, s>>>(e.desc.p, e.data.p, e.rows,
-                                                                         e.base, acc.p);
-    TG_CHECK_LAUNCH();
-    ++g_launches;
-  }
-  unsigned long long h = 0;
-  TG_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
-  TG_CUDA(cudaStreamSynchronize(s));
-  return h;
-}
-
 uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s) {
   DBuf<unsigned long long> acc(1, s);
   acc.zero();

@@ -158,7 +158,6 @@ struct CsrView {
   uint32_t base;
   float avg_len = 0.f;  // host-side hint: mean list length (kernel choice)
   bool quad_ok = false;  // host-side: list slots < 2^34 (32-bit quad indices)
-  bool near_ok = false;  // host-side: most entries lie within 32 ids of their row
 };
 
 // ---- build / orient (build.cu, orient.cu) ----
@@ -187,8 +186,6 @@ void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
                   unsigned long long* cnt, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
-// oriented entries u of row v with |u - v| < 32 (host result).
-uint64_t near_entries(const DevEff& e, cudaStream_t s);
 // sum of the lengths of the lists longer than thr (host result).
 uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s);
 // sum of list lengths over rows [lo, hi) (host result).
