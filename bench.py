@@ -393,6 +393,19 @@ def run_ours(args):
         if i >= args.e2e_warmup:
             e2e_t.append(dt)
     e2e_s = sum(e2e_t) / len(e2e_t)
+    # the PCIe floor on this box: the bare pinned H2D of the same bytes
+    d_off = torch.empty_like(off_p, device="cuda")
+    d_adj = torch.empty_like(adj_p, device="cuda")
+    h2d_t = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d_off.copy_(off_p, non_blocking=True)
+        d_adj.copy_(adj_p, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_t.append(time.perf_counter() - t0)
+    del d_off, d_adj
+    h2d_floor = min(h2d_t)
 
     if rank != 0:
         return
@@ -440,6 +453,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d * ws,
                 "d2h_bytes_per_step": 8 * ws, "ms_per_step": 1e3 * e2e_s,
+                "step_ms": [round(1e3 * x, 3) for x in e2e_t],
+                "h2d_only_ms": 1e3 * h2d_floor,  # bare copy of the same bytes (not the metric)
                 "path": ("tg_count_from_csr(pinned host CSR): chunked H2D overlapped with "
                          "orientation and the count of every apex whose lists arrived"
                          if ws == 1 else
@@ -459,8 +474,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--cpu-parts", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
