@@ -310,6 +310,13 @@ tg_status tg_gen_rmat(uint32_t scale, uint64_t edge_factor, double a, double b, 
 tg_status tg_gen_ws(uint64_t n, uint64_t k, double beta, uint64_t seed, uint32_t** pairs,
                     uint64_t* num_pairs);
 void tg_free_host(void* p);
+/* The same R-MAT / Watts-Strogatz streams generated ON THE DEVICE (one
+ * thread per xoshiro chunk, bit-identical pairs) and built into a graph
+ * there (n = 2^scale / n): no host edge list. */
+tg_status tg_graph_from_rmat(int device, uint32_t scale, uint64_t edge_factor, double a, double b,
+                             double c, uint64_t seed, tg_graph** out);
+tg_status tg_graph_from_ws(int device, uint64_t n, uint64_t k, double beta, uint64_t seed,
+                           tg_graph** out);
 
 #ifdef __cplusplus
 }

@@ -99,6 +99,8 @@ SIGNATURES = {
     "tg_gen_rmat": (_i32, [_u32, _u64, _dbl, _dbl, _dbl, _u64, _pvp, _pu64]),
     "tg_gen_ws": (_i32, [_u64, _u64, _dbl, _u64, _pvp, _pu64]),
     "tg_free_host": (None, [_vp]),
+    "tg_graph_from_rmat": (_i32, [C.c_int, _u32, _u64, _dbl, _dbl, _dbl, _u64, _pvp]),
+    "tg_graph_from_ws": (_i32, [C.c_int, _u64, _u64, _dbl, _u64, _pvp]),
 }
 
 _lib = None

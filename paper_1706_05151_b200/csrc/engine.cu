@@ -520,6 +520,26 @@ tg_status parse_guard(uint64_t* err_line, F&& f) {
 
 }  // namespace
 
+namespace {
+template <class Gen>
+tg_status graph_from_generator(int device, uint64_t n_override, tg_graph** out, Gen&& gen) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr, "null output handle");
+    tg_graph* g = new_graph(device);
+    try {
+      DBuf<uint32_t> pairs;
+      const uint64_t E = gen(pairs, g->stream);
+      tgb::build_graph_device(pairs.p, E, n_override, g->g, g->stream);
+      sync(g);
+    } catch (...) {
+      tg_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+}  // namespace
+
 extern "C" {
 
 const char* tg_last_error(void) { return t_last_error.c_str(); }
@@ -745,6 +765,21 @@ tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, con
       throw;
     }
     cleanup();
+  });
+}
+
+tg_status tg_graph_from_rmat(int device, uint32_t scale, uint64_t edge_factor, double a, double b,
+                             double c, uint64_t seed, tg_graph** out) {
+  const uint64_t n = scale >= 1 && scale <= 31 ? 1ull << scale : 0;
+  return graph_from_generator(device, n, out, [&](DBuf<uint32_t>& pairs, cudaStream_t s) {
+    return tgb::gen_rmat_device(scale, edge_factor, a, b, c, seed, pairs, s);
+  });
+}
+
+tg_status tg_graph_from_ws(int device, uint64_t n, uint64_t k, double beta, uint64_t seed,
+                           tg_graph** out) {
+  return graph_from_generator(device, n, out, [&](DBuf<uint32_t>& pairs, cudaStream_t s) {
+    return tgb::gen_ws_device(n, k, beta, seed, pairs, s);
   });
 }
 

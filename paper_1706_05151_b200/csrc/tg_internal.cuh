@@ -202,6 +202,13 @@ uint64_t parse_edge_list_device(const char* d_text, uint64_t len, DBuf<uint32_t>
 // write_edge_list: "u v\n" for every edge u < v; returns the byte length.
 uint64_t write_edge_list_device(const DevGraph& g, DBuf<char>& out, cudaStream_t s);
 
+// ---- generators (gen.cu): the host harness's R-MAT / Watts-Strogatz
+// streams, bit-identical, into a device pair buffer (returns the pair count)
+uint64_t gen_rmat_device(uint32_t scale, uint64_t edge_factor, double a, double b, double c,
+                         uint64_t seed, DBuf<uint32_t>& pairs, cudaStream_t s);
+uint64_t gen_ws_device(uint64_t n, uint64_t k, double beta, uint64_t seed, DBuf<uint32_t>& pairs,
+                       cudaStream_t s);
+
 // ---- orders (order.cu, order.hpp:39-128) ----
 // Switch g's orientation order to OrderKind{kind, seed}: builds g.okey
 // (the rank array) for non-degree kinds.

@@ -602,6 +602,23 @@ def variance_report(g: Graph, plan: PartitionPlan, q: float) -> VarianceReport:
 # ---------------------------------------------------------------- generators
 
 
+def graph_rmat(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int,
+               device: int = 0) -> Graph:
+    """gen_rmat generated on the device (the same pairs as ``gen_rmat``) and
+    built into a Graph there, n = 2^scale."""
+    h = C.c_void_p()
+    check(lib().tg_graph_from_rmat(device, scale, edge_factor, a, b, c, seed, C.byref(h)))
+    return Graph(h, device)
+
+
+def graph_ws(n: int, k: int, beta: float, seed: int, device: int = 0) -> Graph:
+    """gen_ws generated on the device (the same pairs as ``gen_ws``) and built
+    into a Graph there."""
+    h = C.c_void_p()
+    check(lib().tg_graph_from_ws(device, n, k, beta, seed, C.byref(h)))
+    return Graph(h, device)
+
+
 def normalized_triangle_count(triangles: int, n: int) -> float:
     """stats.hpp:21-23: mean triangles per node."""
     return 0.0 if n == 0 else float(triangles) / float(n)

@@ -133,3 +133,22 @@ def test_device_text_input():
     assert T.parse_edge_list(buf).tolist() == [[0, 1], [1, 2], [2, 0], [2, 3]]
     with T.build_graph_from_text(buf) as g:
         assert T.count_node_iterator_n(g) == 1
+
+
+@pytest.mark.parametrize("kind", ["rmat", "ws"])
+def test_device_generators_match_host(kind):
+    """R-MAT / Watts-Strogatz generated on the device build the same graph as
+    the host harness's pair stream (SURVEY 8(f) #3)."""
+    if kind == "rmat":
+        pairs, n = T.gen_rmat(15, 8, 0.57, 0.19, 0.19, 11), 1 << 15
+        g = T.graph_rmat(15, 8, 0.57, 0.19, 0.19, 11)
+    else:
+        pairs, n = T.gen_ws(200_003, 10, 0.1, 11), 200_003
+        g = T.graph_ws(200_003, 10, 0.1, 11)
+    with T.build_graph(pairs, n) as ref, g:
+        o1, a1 = ref.csr()
+        o2, a2 = g.csr()
+        assert np.array_equal(o1, o2) and np.array_equal(a1, a2)
+        assert T.count_node_iterator_n(g) == T.count_node_iterator_n(ref)
+    with pytest.raises(ValueError):
+        T.graph_ws(10, 3, 0.1, 1)

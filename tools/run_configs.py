@@ -60,12 +60,20 @@ def main():
         if a.small:
             p.update(SMALL[name])
         t0 = time.time()
-        pairs, n = gen(kind, p)
-        t1 = time.time()
-        g = T.build_graph(pairs, n)
-        del pairs
-        torch.cuda.synchronize()
-        t2 = time.time()
+        if os.environ.get("TG_DEVICE_GEN") and kind in ("rmat", "ws"):
+            # generated and built on the device (bit-identical pair streams)
+            g = (T.graph_rmat(p["scale"], p["ef"], 0.57, 0.19, 0.19, p["seed"]) if kind == "rmat"
+                 else T.graph_ws(p["n"], p["k"], p["beta"], p["seed"]))
+            n = g.num_nodes()
+            torch.cuda.synchronize()
+            t1 = t2 = time.time()
+        else:
+            pairs, n = gen(kind, p)
+            t1 = time.time()
+            g = T.build_graph(pairs, n)
+            del pairs
+            torch.cuda.synchronize()
+            t2 = time.time()
         m = g.num_edges()
         W = T.ordering_cost(g)
         s = torch.cuda.Stream()
