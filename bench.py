@@ -367,15 +367,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if dist:
-            h = C.c_void_p()
-            check(L.tg_graph_from_csr(local, n, C.c_void_p(off_p.data_ptr()),
-                                      C.c_void_p(adj_p.data_ptr()), C.byref(h)))
-            part = torch.zeros(1, dtype=torch.int64, device="cuda")
-            check(L.tg_set_stream(h, C.c_void_p(stream.cuda_stream)))
-            check(L.tg_aop_rank_device(h, bptr, ws, rank, C.c_void_p(part.data_ptr())))
+            # this rank's AOP core from its host CSR, streamed the same way
+            c64 = C.c_uint64()
+            check(L.tg_count_from_csr_range(local, n, C.c_void_p(off_p.data_ptr()),
+                                            C.c_void_p(adj_p.data_ptr()), int(plan[rank]),
+                                            int(plan[rank + 1]), C.byref(c64)))
+            part = torch.tensor([c64.value], dtype=torch.int64, device="cuda")
             dist.all_reduce(part)
             cnt = int(part.item())  # 8-byte result back to the host
-            check(L.tg_graph_free(h))
         else:
             # one reference-facing call: Graph(n, offsets, adj) + by_degree
             # orientation + count, the upload streamed under the compute
@@ -458,8 +457,8 @@ def run_ours(args):
                 "path": ("tg_count_from_csr(pinned host CSR): chunked H2D overlapped with "
                          "orientation and the count of every apex whose lists arrived"
                          if ws == 1 else
-                         "per rank: tg_graph_from_csr(pinned host CSR) + tg_aop_rank_device "
-                         "+ NCCL all-reduce + tg_graph_free; max over ranks")},
+                         "per rank: tg_count_from_csr_range(pinned host CSR, its DPD core) "
+                         "+ NCCL all-reduce of the 8-byte counts; max over ranks")},
         "gpu_launches": int(launches),
         "clocks": clk,
     }

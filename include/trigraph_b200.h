@@ -129,6 +129,11 @@ tg_status tg_graph_free(tg_graph* g);
  * pointers fall back to tg_graph_from_csr + tg_count. */
 tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,
                             uint64_t* total);
+/* The same, counting only the apexes in [vlo, vhi): one AOP rank's body
+ * (engines.hpp:38-54) from a host CSR, e.g. core i of a DPD plan. */
+tg_status tg_count_from_csr_range(int device, uint64_t n, const uint64_t* offsets,
+                                  const uint32_t* adj, uint64_t vlo, uint64_t vhi,
+                                  uint64_t* total);
 /* build_graph(parse_edge_list(text), n_override) with both steps on the
  * device (the CLI's --input path, cli.hpp:81-88).  text: len bytes, host or
  * device.  On malformed input: TG_ERR_PARSE, *err_line (may be NULL) = the

@@ -56,6 +56,7 @@ SIGNATURES = {
     "tg_graph_from_edges": (_i32, [C.c_int, _vp, _u64, _u64, _pvp]),
     "tg_graph_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pvp]),
     "tg_count_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pu64]),
+    "tg_count_from_csr_range": (_i32, [C.c_int, _u64, _vp, _vp, _u64, _u64, _pu64]),
     "tg_graph_free": (_i32, [_vp]),
     "tg_graph_info": (_i32, [_vp, _pu64, _pu64]),
     "tg_graph_csr": (_i32, [_vp, _vp, _vp]),

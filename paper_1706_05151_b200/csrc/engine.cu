@@ -674,7 +674,14 @@ tg_status tg_write_edge_list(tg_graph* g, char* out, uint64_t capacity, uint64_t
 
 tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* adj,
                             uint64_t* total) {
+  return tg_count_from_csr_range(device, n, offsets, adj, 0, n, total);
+}
+
+tg_status tg_count_from_csr_range(int device, uint64_t n, const uint64_t* offsets,
+                                  const uint32_t* adj, uint64_t vlo, uint64_t vhi,
+                                  uint64_t* total) {
   return guard([&] {
+    TG_REQUIRE(vlo <= vhi && vhi <= n, "apex range must satisfy vlo <= vhi <= n");
     TG_REQUIRE(total != nullptr && offsets != nullptr, "null argument");
     TG_REQUIRE(n <= 0xFFFFFFFFull, "n must fit NodeId");
     if (is_device_ptr(offsets) || (adj && is_device_ptr(adj))) {
@@ -682,7 +689,21 @@ tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, con
       tg_graph* h = nullptr;
       tg_status st = tg_graph_from_csr(device, n, offsets, adj, &h);
       if (st != TG_OK) throw tgb::Error(st, t_last_error);
-      st = tg_count(h, total);
+      if (vlo == 0 && vhi == n) {
+        st = tg_count(h, total);
+      } else {
+        // AOP rank body over [vlo, vhi) (engines.hpp:38-54): core 1 of a 3-part plan
+        DBuf<unsigned long long> d(1, h->stream);
+        d.zero();
+        const uint32_t plan[4] = {0, (uint32_t)vlo, (uint32_t)vhi, (uint32_t)n};
+        st = tg_aop_rank_device(h, plan, 3, 1, (uint64_t*)d.p);
+        if (st == TG_OK) {
+          unsigned long long v = 0;
+          download(&v, d.p, 1, h->stream);
+          sync(h);
+          *total = v;
+        }
+      }
       const std::string err = t_last_error;
       tg_graph_free(h);
       if (st != TG_OK) throw tgb::Error(st, err);
@@ -746,9 +767,10 @@ tg_status tg_count_from_csr(int device, uint64_t n, const uint64_t* offsets, con
         TG_CUDA(cudaStreamWaitEvent(s, evs[k + 1], 0));
         tgb::orient_chunk(g->g, g->eff, cb[k], cb[k + 1], bigq.p, ctr.p, s);
         tgb::ready_chunks(g->eff, d_cb.p, (uint32_t)K, (uint32_t)k, cb[k], cb[k + 1], ready.p, s);
-        tgb::select_ready(ready.p, cb[k + 1], (uint32_t)k, ids.p, cnt.p, s);
-        if (cb[k + 1])
-          tgb::intersect_list(full, ids.p, cnt.p, cb[k + 1], full,
+        const uint32_t sb = (uint32_t)vlo, se = std::min<uint32_t>(cb[k + 1], (uint32_t)vhi);
+        tgb::select_ready(ready.p, sb, se, (uint32_t)k, ids.p, cnt.p, s);
+        if (se > sb)
+          tgb::intersect_list(full, ids.p, cnt.p, se - sb, full,
                               CountOut{d_total.p, nullptr, nullptr, nullptr, 0}, g->scr, s,
                               g->eff.data.n);
       }

@@ -935,10 +935,10 @@ __global__ void k_ready_chunk(const uint64_t* __restrict__ edesc, const uint32_t
 }
 
 // apexes v < ve whose ready chunk is k (any order)
-__global__ void k_select_ready(const uint8_t* __restrict__ ready, uint32_t ve, uint32_t k,
+__global__ void k_select_ready(const uint8_t* __restrict__ ready, uint32_t vb, uint32_t ve, uint32_t k,
                                uint32_t* __restrict__ ids, unsigned long long* __restrict__ cnt) {
   const unsigned lane = threadIdx.x & 31;
-  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < ve;
+  for (uint64_t base = vb + blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < ve;
        base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = base + lane;
     const bool take = v < ve && ready[v] == k;
@@ -1001,11 +1001,11 @@ void ready_chunks(const DevEff& e, const uint32_t* d_cb, uint32_t K, uint32_t k,
   ++g_launches;
 }
 
-void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
+void select_ready(const uint8_t* ready, uint32_t vb, uint32_t ve, uint32_t k, uint32_t* ids,
                   unsigned long long* cnt, cudaStream_t s) {
   TG_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
-  if (!ve) return;
-  k_select_ready<<<grid_for(ve, 256), 256, 0, s>>>(ready, ve, k, ids, cnt);
+  if (ve <= vb) return;
+  k_select_ready<<<grid_for(ve - vb, 256), 256, 0, s>>>(ready, vb, ve, k, ids, cnt);
   TG_CHECK_LAUNCH();
   ++g_launches;
 }

@@ -175,14 +175,14 @@ void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s);
 // orients vertices [vb, ve) (vb a multiple of 32); ready_chunks records for
 // each apex of chunk k the chunk after which it can be counted (chunk vertex
 // boundaries d_cb, K+1 entries, device); select_ready lists the apexes
-// v < ve whose ready chunk is k into ids, their number into *cnt (device).
+// v in [vb, ve) whose ready chunk is k into ids, their number into *cnt.
 void orient_chunk_begin(const DevGraph& g, DevEff& out, DBuf<uint32_t>& bigq,
                         DBuf<unsigned long long>& ctr, cudaStream_t s);
 void orient_chunk(const DevGraph& g, DevEff& out, uint32_t vb, uint32_t ve, uint32_t* bigq,
                   unsigned long long* ctr, cudaStream_t s);
 void ready_chunks(const DevEff& e, const uint32_t* d_cb, uint32_t K, uint32_t k, uint32_t vb,
                   uint32_t ve, uint8_t* ready, cudaStream_t s);
-void select_ready(const uint8_t* ready, uint32_t ve, uint32_t k, uint32_t* ids,
+void select_ready(const uint8_t* ready, uint32_t vb, uint32_t ve, uint32_t k, uint32_t* ids,
                   unsigned long long* cnt, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);

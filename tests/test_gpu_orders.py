@@ -205,3 +205,35 @@ def test_count_from_csr_streamed(chunk):
             assert T.count_from_csr(ref.n, off_p, adj_p) == want
     finally:
         L.tg_debug_set_chunk_entries(0)
+
+
+def test_count_from_csr_range_is_the_aop_rank_body():
+    """tg_count_from_csr_range over core i of a DPD plan equals the
+    reference's per-rank AOP count (engines.hpp:38-54), streamed from host
+    buffers and from device buffers (no-overlap fallback)."""
+    import ctypes as C
+
+    import torch
+
+    L = lib()
+    pairs = T.gen_pa(20000, 20, 3)
+    ref = O.build_graph(pairs)
+    want = O.run_engine(ref, "aop", 5)
+    d_off = torch.from_numpy(ref.off.view(np.int64)).cuda()
+    d_adj = torch.from_numpy(ref.adj.view(np.int32)).cuda()
+    try:
+        L.tg_debug_set_chunk_entries(4096)
+        for i in range(5):
+            lo, hi = int(want.boundaries[i]), int(want.boundaries[i + 1])
+            t = C.c_uint64()
+            check(L.tg_count_from_csr_range(0, ref.n, C.c_void_p(ref.off.ctypes.data),
+                                            C.c_void_p(ref.adj.ctypes.data), lo, hi, C.byref(t)))
+            assert t.value == int(want.triangles[i])
+            check(L.tg_count_from_csr_range(0, ref.n, C.c_void_p(d_off.data_ptr()),
+                                            C.c_void_p(d_adj.data_ptr()), lo, hi, C.byref(t)))
+            assert t.value == int(want.triangles[i])
+        with pytest.raises(ValueError):
+            check(L.tg_count_from_csr_range(0, ref.n, C.c_void_p(ref.off.ctypes.data),
+                                            C.c_void_p(ref.adj.ctypes.data), 5, 2, C.byref(t)))
+    finally:
+        L.tg_debug_set_chunk_entries(0)
