@@ -120,6 +120,49 @@ def _all_to_allv(t: torch.Tensor, send_counts: List[int], recv_counts: List[int]
     return out
 
 
+def gather_host_csr(n: int, offsets: torch.Tensor, adj: torch.Tensor, device,
+                    group=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Every rank ends with the full CSR (Graph, graph.hpp:19-53) in its HBM,
+    having copied only 1/p of it over its own host link: rank r uploads slice
+    r of the offsets and of the adjacency (pinned host tensors -> HBM), then
+    one all-gather per array assembles the rest over NVLink (NCCL) -- the
+    CSR is replicated for AOP (engines.hpp:38-54), and the host link, not
+    NVLink, is the narrow one.  Returns (offsets int64[n+1], adj int32[2m])
+    views on `device`."""
+    p = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    out = []
+    for src, count in ((offsets, n + 1), (adj, adj.numel())):
+        chunk = max(1, -(-count // p))  # equal slices (NCCL all-gather), last one padded
+        full = torch.empty(p * chunk, dtype=src.dtype, device=device)
+        mine = torch.zeros(chunk, dtype=src.dtype, device=device)
+        a0 = min(count, rank * chunk)
+        a1 = min(count, a0 + chunk)
+        if a1 > a0:
+            mine[: a1 - a0].copy_(src[a0:a1], non_blocking=True)
+        dist.all_gather_into_tensor(full, mine, group=group)
+        out.append(full[:count])
+    return out[0], out[1]
+
+
+def count_aop_from_host_csr(n: int, offsets: torch.Tensor, adj: torch.Tensor, b: np.ndarray,
+                            device, group=None) -> int:
+    """AOP (engines.hpp:38-54) end to end from host buffers on every rank:
+    gather_host_csr, then this rank's core [b_r, b_r+1) counted on its GPU
+    (tg_count_from_csr_range), then the one all-reduce of T."""
+    rank = dist.get_rank(group)
+    d_off, d_adj = gather_host_csr(n, offsets, adj, device, group)
+    torch.cuda.current_stream(device).synchronize()
+    t = C.c_uint64()
+    check(lib().tg_count_from_csr_range(torch.device(device).index or 0, n,
+                                        C.c_void_p(d_off.data_ptr()),
+                                        C.c_void_p(d_adj.data_ptr()) if d_adj.numel() else None,
+                                        int(b[rank]), int(b[rank + 1]), C.byref(t)))
+    total = torch.tensor([t.value], dtype=torch.int64, device=device)
+    dist.all_reduce(total, group=group)
+    return int(total.item())
+
+
 def run_engine_distributed(backend: RankBackend, engine: EngineKind = EngineKind.Aop,
                            cost: CostKind = CostKind.Dpd, group=None) -> RunReport:
     """run_engine (engines.hpp:335-418) with ranks = the process group."""

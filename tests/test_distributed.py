@@ -134,3 +134,35 @@ def test_distributed_engines_match_reference_semantics(world):
             assert [x[0] for x in per] == want.triangles.tolist()
             assert [x[1] for x in per] == want.data_sent.tolist()
             assert [x[2] for x in per] == want.data_recv.tolist()
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        g = O.random_graph(97, 0.2, 5)
+        off = torch.from_numpy(g.off.view(np.int64))
+        adj = torch.from_numpy(g.adj.view(np.int32))
+        d_off, d_adj = D.gather_host_csr(g.n, off, adj, torch.device("cpu"))
+        q.put((rank, bool(torch.equal(d_off, off) and torch.equal(d_adj, adj))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sliced_upload_gather_reassembles_the_csr(world):
+    """distributed.gather_host_csr (the N > 1 e2e path): each rank ships
+    1/world of the arrays; after the all-gather every rank holds them whole
+    (slices padded to equal sizes for the collective)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(results.values())

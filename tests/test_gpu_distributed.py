@@ -34,5 +34,14 @@ def test_nccl_single_rank_driver():
             rep = D.run_engine_distributed(be, engine, T.CostKind.Dpd)
             assert rep.total == want
             assert rep.per_rank[0].triangles == want and rep.per_rank[0].data_sent == 0
+        # the e2e path of bench.py at N > 1: sliced upload + NCCL all-gather
+        # + this rank's AOP core (the whole graph with one rank)
+        off_p = torch.from_numpy(ref.off.view("int64")).pin_memory()
+        adj_p = torch.from_numpy(ref.adj.view("int32")).pin_memory()
+        d_off, d_adj = D.gather_host_csr(ref.n, off_p, adj_p, torch.device("cuda", 0))
+        assert torch.equal(d_off.cpu(), off_p) and torch.equal(d_adj.cpu(), adj_p)
+        plan = T.compute_boundaries(g, T.CostKind.Dpd, 1).boundaries
+        assert D.count_aop_from_host_csr(ref.n, off_p, adj_p, plan,
+                                         torch.device("cuda", 0)) == want
     finally:
         dist.destroy_process_group()
