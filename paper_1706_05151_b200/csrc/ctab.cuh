@@ -16,8 +16,12 @@
 // exceeds the capacity stay on k_intersect_ctaq.
 #pragma once
 
+#ifndef TG_CTAB_MINB
+#define TG_CTAB_MINB 2
+#endif
+
 template <bool TALLY, bool LIST, bool FILTER, class Apex>
-__global__ void __launch_bounds__(kCT, 2)
+__global__ void __launch_bounds__(kCT, TG_CTAB_MINB)
 k_intersect_ctab(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
                  const uint32_t* __restrict__ big, const unsigned long long* __restrict__ big_count,
                  uint64_t big_cap, RankView rv, unsigned long long* __restrict__ work_ctr) {
