@@ -251,6 +251,17 @@ tg_status tg_count_device(tg_graph* g, uint64_t* d_total);
 /* AOP rank body: count triangles whose apex lies in core `rank`. */
 tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p,
                              uint64_t rank, uint64_t* d_total);
+/* The AOP rank body with the reference's sinks (engines.hpp:303-321
+ * RankSink): d_tally (n uint64, device, accumulated; may be NULL) gets
+ * T_v += 1 at the three corners of every triangle whose apex is in core
+ * `rank`; d_tri (3*capacity uint32, device; may be NULL) the triples
+ * (ascending ids) at positions claimed from *d_cursor (device uint64). */
+tg_status tg_aop_rank_sinks_device(tg_graph* g, const uint32_t* boundaries, uint64_t p,
+                                   uint64_t rank, uint64_t* d_total, uint64_t* d_tally,
+                                   uint32_t* d_tri, uint64_t capacity, uint64_t* d_cursor);
+/* clustering coefficients (engines.hpp:258-267) of device tallies (n uint64)
+ * into d_cc (n fp64, device), IEEE-rounded like tg_clustering_coefficients. */
+tg_status tg_cc_from_tally_device(tg_graph* g, const uint64_t* d_tally, double* d_cc);
 /* Surrogate pack (engines.hpp:173-187): sizes first (host sync).
  * msgs_per_dest / words_per_dest: p entries each (host). */
 tg_status tg_surrogate_pack_sizes(tg_graph* g, const uint32_t* boundaries, uint64_t p,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "tg_orient_device": (_i32, [_vp]),
     "tg_count_device": (_i32, [_vp, _vp]),
     "tg_aop_rank_device": (_i32, [_vp, _vp, _u64, _u64, _vp]),
+    "tg_aop_rank_sinks_device": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp, _vp, _u64, _vp]),
+    "tg_cc_from_tally_device": (_i32, [_vp, _vp, _vp]),
     "tg_surrogate_pack_sizes": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "tg_surrogate_pack_device": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "tg_surrogate_count_device": (_i32, [_vp, _vp, _u64, _u64, _vp, _u64, _vp, _vp]),

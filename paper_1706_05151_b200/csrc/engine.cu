@@ -1216,6 +1216,37 @@ tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p
   });
 }
 
+tg_status tg_aop_rank_sinks_device(tg_graph* g, const uint32_t* boundaries, uint64_t p,
+                                   uint64_t rank, uint64_t* d_total, uint64_t* d_tally,
+                                   uint32_t* d_tri, uint64_t capacity, uint64_t* d_cursor) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(boundaries && p >= 1 && rank < p && d_total, "invalid argument");
+    TG_REQUIRE(boundaries[0] == 0 && boundaries[p] <= g->g.n, "invalid boundaries");
+    TG_REQUIRE(!d_tri || d_cursor, "listing needs a cursor");
+    ensure_eff(g);
+    cudaStream_t s = g->stream;
+    const CsrView full = view(g->eff);
+    const uint32_t N = (uint32_t)g->g.n;
+    const uint32_t cb = boundaries[rank], ce = boundaries[rank + 1];
+    timed_pass(g, [&] {
+      if (ce > cb)
+        tgb::intersect_rows(full, cb, ce, full, 0, N,
+                            CountOut{(unsigned long long*)d_total, (unsigned long long*)d_tally,
+                                     d_tri, (unsigned long long*)d_cursor, capacity},
+                            g->scr, s, g->eff.data.n, true, rank_view(g));
+    });
+  });
+}
+
+tg_status tg_cc_from_tally_device(tg_graph* g, const uint64_t* d_tally, double* d_cc) {
+  return guard([&] {
+    enter(g);
+    TG_REQUIRE(d_tally && d_cc, "null argument");
+    tgb::clustering_device(g->g, (const unsigned long long*)d_tally, d_cc, g->stream);
+  });
+}
+
 tg_status tg_surrogate_pack_sizes(tg_graph* g, const uint32_t* boundaries, uint64_t p, uint64_t rank,
                                   uint64_t* msgs_per_dest, uint64_t* words_per_dest) {
   return guard([&] {

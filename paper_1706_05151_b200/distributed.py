@@ -54,6 +54,20 @@ class RankBackend:
                         data: torch.Tensor) -> int:
         raise NotImplementedError
 
+    def aop_tally(self, b: np.ndarray, rank: int) -> torch.Tensor:
+        """int64[n]: T_v over the triangles whose apex is in core `rank`,
+        counted at all three corners (RankSink tallies, engines.hpp:303-321)."""
+        raise NotImplementedError
+
+    def cc(self, tally: torch.Tensor) -> torch.Tensor:
+        """float64[n]: C_v = 2 T_v / (d (d - 1)), 0 for d < 2 (engines.hpp:258-267)."""
+        raise NotImplementedError
+
+    def aop_list(self, b: np.ndarray, rank: int) -> torch.Tensor:
+        """int32[k, 3]: the triangles whose apex is in core `rank`, ascending ids
+        per triple (ListSink normalisation, sequential.hpp:39-44)."""
+        raise NotImplementedError
+
 
 class CudaRankBackend(RankBackend):
     """This rank's GPU through the C ABI (Graph resident on `device`)."""
@@ -110,6 +124,42 @@ class CudaRankBackend(RankBackend):
         return int(self._acc.item())
 
 
+    def aop_tally(self, b, rank):
+        b = np.ascontiguousarray(b, dtype=np.uint32)
+        n = self.g.num_nodes()
+        tv = torch.zeros(max(n, 1), dtype=torch.int64, device=self.device)
+        self._acc.zero_()
+        self._sync()
+        check(lib().tg_aop_rank_sinks_device(self.g._h, C.c_void_p(b.ctypes.data), len(b) - 1,
+                                             rank, C.c_void_p(self._acc.data_ptr()),
+                                             C.c_void_p(tv.data_ptr()), None, 0, None))
+        self._sync()
+        return tv[:n]
+
+    def cc(self, tally):
+        n = self.g.num_nodes()
+        out = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
+        if n:
+            check(lib().tg_cc_from_tally_device(self.g._h, C.c_void_p(tally.data_ptr()),
+                                                C.c_void_p(out.data_ptr())))
+        self._sync()
+        return out[:n]
+
+    def aop_list(self, b, rank):
+        k = self.aop_count(b, rank)
+        b = np.ascontiguousarray(b, dtype=np.uint32)
+        tri = torch.empty((max(k, 1), 3), dtype=torch.int32, device=self.device)
+        cur = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._acc.zero_()
+        self._sync()
+        check(lib().tg_aop_rank_sinks_device(self.g._h, C.c_void_p(b.ctypes.data), len(b) - 1,
+                                             rank, C.c_void_p(self._acc.data_ptr()), None,
+                                             C.c_void_p(tri.data_ptr()), k,
+                                             C.c_void_p(cur.data_ptr())))
+        self._sync()
+        return tri[:k]
+
+
 def _all_to_allv(t: torch.Tensor, send_counts: List[int], recv_counts: List[int],
                  group=None) -> torch.Tensor:
     out = torch.empty(sum(recv_counts), dtype=t.dtype, device=t.device)
@@ -163,6 +213,49 @@ def count_aop_from_host_csr(n: int, offsets: torch.Tensor, adj: torch.Tensor, b:
     return int(total.item())
 
 
+def _shared_plan(backend: RankBackend, cost: CostKind, group) -> np.ndarray:
+    """The cost-function plan (partition.hpp:116-141); every rank derives the
+    same one, rank 0's copy is authoritative."""
+    p = dist.get_world_size(group)
+    b = np.ascontiguousarray(backend.plan(cost, p), dtype=np.uint32)
+    bt = torch.from_numpy(b.astype(np.int64)).to(backend.device)
+    dist.broadcast(bt, 0, group=group)
+    return bt.cpu().numpy().astype(np.uint32)
+
+
+def clustering_distributed(backend: RankBackend, cost: CostKind = CostKind.Dpd, group=None):
+    """clustering_coefficients (engines.hpp:422-435) with ranks = the process
+    group, AOP: each rank tallies the triangles of its core apexes at all
+    three corners into a full n-vector on its GPU, one all-reduce sums them
+    (the owner-side aggregation of engines.hpp:229-254, done for every vertex
+    at once), and C_v is computed on the device.  Every rank returns the same
+    (total, T_v uint64[n], C_v float64[n])."""
+    rank = dist.get_rank(group)
+    b = _shared_plan(backend, cost, group)
+    tv = backend.aop_tally(b, rank)
+    dist.all_reduce(tv, group=group)
+    cc = backend.cc(tv)
+    tvh = tv.cpu().numpy().astype(np.uint64)
+    return int(tvh.sum()) // 3, tvh, cc.cpu().numpy()
+
+
+def list_triangles_distributed(backend: RankBackend, cost: CostKind = CostKind.Dpd, group=None):
+    """Triangle listing (collect_triangles, engines.hpp:313-319) with ranks =
+    the process group, AOP: each rank lists the triangles of its core apexes
+    into a buffer on its own GPU; an all-gather of the per-rank counts gives
+    each rank its offset in the global list.  Returns (local int32[k, 3] on
+    this rank's device, offset, total)."""
+    p = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    b = _shared_plan(backend, cost, group)
+    tri = backend.aop_list(b, rank)
+    k = torch.tensor([tri.shape[0]], dtype=torch.int64, device=backend.device)
+    ks = [torch.empty_like(k) for _ in range(p)]
+    dist.all_gather(ks, k, group=group)
+    counts = [int(x.item()) for x in ks]
+    return tri, sum(counts[:rank]), sum(counts)
+
+
 def run_engine_distributed(backend: RankBackend, engine: EngineKind = EngineKind.Aop,
                            cost: CostKind = CostKind.Dpd, group=None) -> RunReport:
     """run_engine (engines.hpp:335-418) with ranks = the process group."""
@@ -171,11 +264,7 @@ def run_engine_distributed(backend: RankBackend, engine: EngineKind = EngineKind
     dev = backend.device
     if engine not in (EngineKind.Aop, EngineKind.AnopSurrogate):
         raise ValueError("distributed engines: Aop and AnopSurrogate")
-    # every rank derives the same plan; rank 0's copy is authoritative
-    b = np.ascontiguousarray(backend.plan(cost, p), dtype=np.uint32)
-    bt = torch.from_numpy(b.astype(np.int64)).to(dev)
-    dist.broadcast(bt, 0, group=group)
-    b = bt.cpu().numpy().astype(np.uint32)
+    b = _shared_plan(backend, cost, group)
     sent = recv = 0
     if engine == EngineKind.Aop:
         tri = backend.aop_count(b, rank)

@@ -61,6 +61,27 @@ class OracleRankBackend(D.RankBackend):
         return (msgs, words, torch.tensor(hdr, dtype=torch.int32),
                 torch.tensor(dat, dtype=torch.int32))
 
+    def _core_triangles(self, b, rank):
+        for v in range(int(b[rank]), int(b[rank + 1])):
+            nv = self.lst(v)
+            for u in nv:
+                for w in np.intersect1d(nv, self.lst(u), assume_unique=True):
+                    yield v, int(u), int(w)
+
+    def aop_tally(self, b, rank):
+        tv = torch.zeros(self.g.n, dtype=torch.int64)
+        for t in self._core_triangles(b, rank):
+            for x in t:
+                tv[x] += 1
+        return tv
+
+    def cc(self, tally):
+        return torch.from_numpy(O.clustering(self.g, tally.numpy().astype(np.uint64)))
+
+    def aop_list(self, b, rank):
+        rows = [sorted(t) for t in self._core_triangles(b, rank)]
+        return torch.tensor(rows, dtype=torch.int32).reshape(-1, 3)
+
     def surrogate_count(self, b, rank, hdr, nmsgs, data):
         cb, ce = int(b[rank]), int(b[rank + 1])
         t = 0
@@ -166,3 +187,53 @@ def test_sliced_upload_gather_reassembles_the_csr(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(results.values())
+
+
+def _sinks_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = O.random_graph(60, 0.3, 17)
+        be = OracleRankBackend(g)
+        total, tv, cc = D.clustering_distributed(be, CostKind.Dpd)
+        tri, off, tot2 = D.list_triangles_distributed(be, CostKind.Dpd)
+        q.put((rank, total, tv.tolist(), cc.tolist(), tri.numpy().tolist(), off, tot2))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_tallies_cc_and_listing(world):
+    """clustering_distributed / list_triangles_distributed:
+    every rank returns the reference's T_v and C_v; the per-rank listings,
+    placed at their all-gathered offsets, are exactly the triangle list."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sinks_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=240)
+        res[r[0]] = r[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = O.random_graph(60, 0.3, 17)
+    T, want_tv, want_tri = O.count(g, tally=True, listing=True)
+    want_cc = O.clustering(g, want_tv)
+    parts = [None] * world
+    for r in range(world):
+        total, tv, cc, tri, off, tot2 = res[r]
+        assert total == T == tot2
+        assert tv == want_tv.tolist()
+        assert np.array_equal(np.array(cc), want_cc)
+        parts[r] = (off, tri)
+    allt = []
+    for off, tri in sorted(parts, key=lambda x: x[0]):
+        assert off == len(allt)
+        allt += tri
+    got = np.array(allt, dtype=np.uint32).reshape(-1, 3)
+    got = got[np.lexsort((got[:, 2], got[:, 1], got[:, 0]))]
+    assert np.array_equal(got, want_tri)

@@ -6,6 +6,7 @@ emulated ranks in tests/test_gpu_parity.py::test_device_step_and_rank_entries.""
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
@@ -43,5 +44,16 @@ def test_nccl_single_rank_driver():
         plan = T.compute_boundaries(g, T.CostKind.Dpd, 1).boundaries
         assert D.count_aop_from_host_csr(ref.n, off_p, adj_p, plan,
                                          torch.device("cuda", 0)) == want
+        # per-vertex counts / clustering coefficients and the
+        # listing through the multi-process driver
+        _, want_tv, want_tri = O.count(ref, tally=True, listing=True)
+        total, tv, cc = D.clustering_distributed(be, T.CostKind.Dpd)
+        assert total == want and np.array_equal(tv, want_tv)
+        assert np.array_equal(cc, O.clustering(ref, want_tv))
+        tri, off, tot = D.list_triangles_distributed(be, T.CostKind.Dpd)
+        assert (off, tot) == (0, want)
+        got = tri.cpu().numpy().view(np.uint32)
+        got = got[np.lexsort((got[:, 2], got[:, 1], got[:, 0]))]
+        assert np.array_equal(got, want_tri)
     finally:
         dist.destroy_process_group()
