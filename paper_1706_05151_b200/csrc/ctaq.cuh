@@ -17,7 +17,10 @@
 // the table would not fit) so that the hash probes run on full warps.
 #pragma once
 
-constexpr int kCQUnroll = 2;
+#ifndef TG_CQUNROLL
+#define TG_CQUNROLL 4
+#endif
+constexpr int kCQUnroll = TG_CQUNROLL;  // quad chunks in flight per warp (ctaq, ctab)
 
 template <bool TALLY, bool LIST, bool FILTER, class Apex>
 __global__ void __launch_bounds__(kCT, 2)

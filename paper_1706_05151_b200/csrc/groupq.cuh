@@ -10,7 +10,10 @@
 // top hash bits, bits from hash bits 0..4 and 5..9.
 #pragma once
 
-constexpr int kGQUnroll = 2;
+#ifndef TG_GQUNROLL
+#define TG_GQUNROLL 2
+#endif
+constexpr int kGQUnroll = TG_GQUNROLL;
 
 __device__ __forceinline__ uint32_t gq_hash(uint32_t x, uint32_t akey) {
   return (x ^ akey) * 0x2545F491u;  // akey = slot * 0x9E3779B9

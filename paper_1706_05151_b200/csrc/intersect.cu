@@ -147,7 +147,10 @@ constexpr int kTblWords = 32;   // segment-start table window: 1024 items
 #ifndef TG_WBLOCKS
 #define TG_WBLOCKS 6
 #endif
-constexpr int kUnroll = 4;      // chunks (of 32 items) in flight per warp (group kernel)
+#ifndef TG_GUNROLL
+#define TG_GUNROLL 4
+#endif
+constexpr int kUnroll = TG_GUNROLL;  // chunks (of 32 items) in flight per warp (group kernel)
 constexpr int kWUnroll = TG_UNROLL;  // ... in the per-apex warp kernel
 constexpr int kWBlocks = TG_WBLOCKS; // resident blocks per SM of the per-apex warp kernel
 constexpr uint32_t kWarpWork = 4096;  // items of the first u-batch above which
