@@ -221,8 +221,9 @@ k_intersect_group(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             as[q] = __shfl_sync(FULL, my_a, jj);
             const uint32_t idx = base + lane;
             jjs[q] = jj;
-            if (WIDE) xs[q] = idx < S ? __ldg(nu.data + ((long long)ad + idx)) : kNoItem;
-            else xs[q] = idx < S ? __ldg(nu.data + (uint32_t)((uint32_t)ad + idx)) : kNoItem;
+            // (idx < wend, not S: items past the window are the next window's)
+            if (WIDE) xs[q] = idx < wend ? __ldg(nu.data + ((long long)ad + idx)) : kNoItem;
+            else xs[q] = idx < wend ? __ldg(nu.data + (uint32_t)((uint32_t)ad + idx)) : kNoItem;
           }
           unsigned hits = 0;
 #pragma unroll

@@ -186,7 +186,9 @@ k_intersect_groupq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             const uint32_t base = base0 + 32 * q;
             const uint32_t word = Tbl[(base - w0) >> 5];
             const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
-            cnt += __popc(word);
+            // only words inside the window: the next window's first segment start
+            // (marked at word kTblWords) is counted there
+            cnt += base < wend ? __popc(word) : 0u;
             jjs[q] = jj;
             const uint32_t qs = __shfl_sync(FULL, my_qs, jj);
             aks[q] = __shfl_sync(FULL, my_a, jj) * 0x9E3779B9u;
@@ -215,7 +217,9 @@ k_intersect_groupq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             const uint32_t aa = __shfl_sync(FULL, my_a, jjs[q]);
             const bool first = (word >> lane) & 1u;
             const bool last = lane < 31 ? ((word >> (lane + 1)) & 1u) : (nxt & 1u);
-            unsigned vm = base + lane < S ? 0xFu : 0u;
+            // items past this window belong to the next one (an unroll that
+            // does not divide the window can reach them): not ours
+            unsigned vm = base + lane < wend ? 0xFu : 0u;
             if (first) vm &= (0xFu << (hts & 3u)) & 0xFu;
             if (last) vm &= 0xFu >> (hts >> 2);
             const unsigned hq = (hb >> (4 * q)) & vm;

@@ -341,8 +341,8 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             const Adj a = __shfl_sync(FULL, my_adj, jj);  // srcLane is taken mod 32
             const uint32_t idx = base + lane;
             jjs[q] = jj;
-            if (WIDE) xs[q] = idx < S ? __ldg(nu.data + ((long long)a + idx)) : kNoItem;
-            else xs[q] = idx < S ? __ldg(nu.data + (uint32_t)((uint32_t)a + idx)) : kNoItem;
+            if (WIDE) xs[q] = idx < wend ? __ldg(nu.data + ((long long)a + idx)) : kNoItem;
+            else xs[q] = idx < wend ? __ldg(nu.data + (uint32_t)((uint32_t)a + idx)) : kNoItem;
           }
           // filter: one conflict-light LDS.32 per item
           unsigned hits = 0;

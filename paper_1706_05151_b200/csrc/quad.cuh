@@ -149,7 +149,9 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             const uint32_t base = base0 + 32 * q;
             const uint32_t word = Tbl[(base - w0) >> 5];
             const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
-            cnt += __popc(word);  // (S's marker only counts past the last item)
+            // only words inside the window: the next window's first segment start
+            // (marked at word kTblWords) is counted there
+            cnt += base < wend ? __popc(word) : 0u;
             jjs[q] = jj;
             const uint32_t qs = __shfl_sync(FULL, my_qs, jj);
             // lanes past S re-read an in-bounds quad; validity is applied
@@ -174,7 +176,7 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             const uint32_t hts = __shfl_sync(FULL, my_ht, jjs[q]);
             const bool first = (word >> lane) & 1u;
             const bool last = lane < 31 ? ((word >> (lane + 1)) & 1u) : (nxt & 1u);
-            unsigned vm = base + lane < S ? 0xFu : 0u;
+            unsigned vm = base + lane < wend ? 0xFu : 0u;  // (this window only)
             if (first) vm &= (0xFu << (hts & 3u)) & 0xFu;
             if (last) vm &= 0xFu >> (hts >> 2);
             const uint32_t xq[4] = {r[q].x, r[q].y, r[q].z, r[q].w};
