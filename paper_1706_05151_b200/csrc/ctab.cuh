@@ -135,7 +135,7 @@ k_intersect_ctab(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
               jjs[q] = jj;
               if (idx < wend) {
                 qix[q] = sQs[jj] + idx;
-                r[q] = __ldg(R4 + qix[q]);
+                r[q] = ldg_cq4(R4 + qix[q]);
                 const uint32_t hts = sHt2[jj];
                 const bool first = (word >> lane) & 1u;
                 const bool last = lane < 31 ? ((word >> (lane + 1)) & 1u) : (nxt & 1u);

@@ -158,7 +158,7 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
               const uint32_t idx = w0 + 32 * ch + lane;
               jjs[q] = jj;
               if (idx < wend) {
-                r[q] = __ldg(Q4 + (sQs[jj] + idx));
+                r[q] = ldg_cq4(Q4 + (sQs[jj] + idx));
                 const uint32_t hts = sHt2[jj];
                 const bool first = (word >> lane) & 1u;
                 const bool last = lane < 31 ? ((word >> (lane + 1)) & 1u) : (nxt & 1u);

@@ -193,7 +193,7 @@ k_intersect_groupq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             const uint32_t qs = __shfl_sync(FULL, my_qs, jj);
             aks[q] = __shfl_sync(FULL, my_a, jj) * 0x9E3779B9u;
             const uint32_t idx = min(base + lane, S - 1);
-            r[q] = __ldg(Q4 + (qs + idx));
+            r[q] = ldg_cq4(Q4 + (qs + idx));
           }
           unsigned hb = 0;  // filter hits, 4 bits per chunk
 #pragma unroll

@@ -18,6 +18,31 @@
 #endif
 constexpr int kQUnroll = TG_QUNROLL;  // quad chunks (32 lanes x 16 B) in flight per warp
 
+// N_u quads almost never hit L1 (ncu: 2.4% sector hit rate), so they are
+// loaded without L1 allocation: C2 intersection 7.63 -> 7.30 ms (A/B of the
+// two builds on one B200, two runs each; -DTG_QUAD_NO_L1=0 restores __ldg).
+#ifndef TG_QUAD_NO_L1
+#define TG_QUAD_NO_L1 1
+#endif
+// the same for the group / CTA quad kernels (ctaq, groupq, ctab)
+#ifndef TG_CQ_NO_L1
+#define TG_CQ_NO_L1 0
+#endif
+template <bool NA>
+__device__ __forceinline__ uint4 ldg_quad(const uint4* p) {
+  if constexpr (NA) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+  } else {
+    return __ldg(p);
+  }
+}
+__device__ __forceinline__ uint4 ldg_stream4(const uint4* p) { return ldg_quad<TG_QUAD_NO_L1 != 0>(p); }
+__device__ __forceinline__ uint4 ldg_cq4(const uint4* p) { return ldg_quad<TG_CQ_NO_L1 != 0>(p); }
+
 template <bool TALLY, bool LIST, bool FILTER, class Apex>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, kWBlocks)
 k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
@@ -157,7 +182,7 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             // lanes past S re-read an in-bounds quad; validity is applied
             // only on the (rare) exact path below
             const uint32_t idx = min(base + lane, S - 1);
-            r[q] = __ldg(Q4 + (qs + idx));
+            r[q] = ldg_stream4(Q4 + (qs + idx));
           }
           // filter over all loaded slots (head/tail slots included)
           bool p = false;
