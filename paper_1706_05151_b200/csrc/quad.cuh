@@ -24,7 +24,9 @@ constexpr int kQUnroll = TG_QUNROLL;  // quad chunks (32 lanes x 16 B) in flight
 #ifndef TG_QUAD_NO_L1
 #define TG_QUAD_NO_L1 1
 #endif
-// the same for the group / CTA quad kernels (ctaq, groupq, ctab)
+// the same for the group / CTA quad kernels (ctaq, groupq, ctab): off -- on C3
+// (R-MAT-24) it measured 225.0 vs 223.0 ms (two runs each), the hub lists
+// those kernels re-read do hit L1
 #ifndef TG_CQ_NO_L1
 #define TG_CQ_NO_L1 0
 #endif
