@@ -30,6 +30,11 @@ constexpr int kQUnroll = TG_QUNROLL;  // quad chunks (32 lanes x 16 B) in flight
 #ifndef TG_CQ_NO_L1
 #define TG_CQ_NO_L1 0
 #endif
+// list descriptors DO hit L1: the no-allocate hint on them measured 7.79 vs
+// 7.29 ms on C2, so it stays off (experiment macro only)
+#ifndef TG_DESC_NO_L1
+#define TG_DESC_NO_L1 0
+#endif
 template <bool NA>
 __device__ __forceinline__ uint4 ldg_quad(const uint4* p) {
   if constexpr (NA) {
@@ -117,7 +122,12 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       uint32_t nq = 0, u = 0, qs0 = 0, ht = 0;
       if (j < jhi) {
         u = Nv[j];
+#if TG_DESC_NO_L1
+        uint64_t d;
+        asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(d) : "l"(nu.desc + (u - nu.base)));
+#else
         const uint64_t d = nu.desc[u - nu.base];
+#endif
         const uint32_t len = desc_len(d);
         const uint64_t lo = desc_start(d), end = lo + len;  // slots < 2^34
         qs0 = (uint32_t)(lo >> 2);
