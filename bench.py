@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """bench.py -- exact triangle counting on B200: oriented edges/s + HBM roofline.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-C2 = preferential attachment PA(n=1e7, 20 attachments/vertex), i.e. the
-reference's gen_pa(1e7, 40, seed=7) edge stream (io.hpp:129-162), ~2e8
-undirected edges, generated bit-identically on the host (synthetic data).
+Workload (--config, default C5): BASELINE.json's largest configuration that
+fits one B200, C5 = preferential attachment PA(n=1e8, 20 attachments/vertex),
+the reference generator's own edge stream gen_pa(1e8, 40, seed=7)
+(io.hpp:129-162), ~2e9 undirected edges, generated bit-identically on the
+host (synthetic data; the other configs C1-C4 are selectable and are parity
+cases in tests/).
 
 A step = one pass of the hot path over the graph resident in HBM:
 degree-ordered orientation (effective_adjacency, effective.hpp:37-52) +
@@ -20,10 +22,17 @@ oriented on arrival and every apex counted as soon as all its lists are
 resident; 8-byte result back) per step, timed with the host clock around
 synchronised calls.
 
---impl reference: the reference's own CPU implementation (oracle/_ref, the
-unmodified trigraph headers) on all host cores: the AOP rank bodies
-build_overlap_partition + aop_count on std::threads over a rotating sample
-of a 256-part DPD plan of the same graph.
+cpu_baseline / --impl reference: the reference's own code
+(oracle/_ref: the unmodified trigraph headers) on the host cores, on the
+oracle-built EffectiveAdjacency of the same graph (setup, untimed):
+  * all cores: the reference AOP through its public API with p = nproc --
+    each std::thread runs build_overlap_partition (partition.hpp:171-206,
+    timed separately) then aop_count (engines.hpp:38-54, the counting phase,
+    the value) on a rotating cost-balanced sub-range of its DPD core;
+  * one thread: count_node_iterator_n's loop (sequential.hpp:74-91, the
+    reference's intersect_visit) over the same sub-ranges.
+The reference arm never loads libtrigraph_b200.so: its input is made by the
+oracle's generators (oracle/fullsize.c).
 """
 from __future__ import annotations
 
@@ -42,8 +51,24 @@ sys.path.insert(0, ROOT)
 
 METRIC = "exact triangle count: oriented edges/sec + achieved HBM GB/s at 1/2/4/8 B200"
 UNIT = "oriented edges/s"
-WORKLOAD = "C2: PA(n=1e7, d=20 attachments) = gen_pa(1e7, 40, seed=7), ~2e8 edges"
-N_NODES, PA_D, SEED = 10_000_000, 40, 7
+CONFIGS = {  # BASELINE.json configs[0..4]
+    "C1": ("gnm", dict(n=100_000, m=1_000_000, seed=1),
+           "C1: Erdos-Renyi G(n=1e5, m=1e6), seed 1"),
+    "C2": ("pa", dict(n=10_000_000, d=40, seed=7),
+           "C2: PA(n=1e7, d=20 attachments) = gen_pa(1e7, 40, seed=7), ~2e8 edges"),
+    "C3": ("rmat", dict(scale=24, ef=16, a=0.57, b=0.19, c=0.19, seed=1),
+           "C3: R-MAT scale 24, edge factor 16, (0.57,0.19,0.19,0.05), seed 1, ~2.6e8 edges"),
+    "C4": ("ws", dict(n=50_000_000, k=20, beta=0.1, seed=1),
+           "C4: Watts-Strogatz n=5e7, k=20, beta=0.1, seed 1, ~5e8 edges"),
+    "C5": ("pa", dict(n=100_000_000, d=40, seed=7),
+           "C5: PA(n=1e8, d=20 attachments) = gen_pa(1e8, 40, seed=7), ~2e9 edges "
+           "(largest BASELINE config; fits one B200)"),
+}
+DEFAULT_CONFIG = "C5"
+TRAFFIC_PROFILES = {  # ncu --set full captures of the intersection pass (profiles/)
+    "C2": "profiles/ncu_intersect.json",
+    "C5": "profiles/ncu_intersect_C5.json",
+}
 
 
 def log(*a):
@@ -55,6 +80,13 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 # ------------------------------------------------------------------ clocks
@@ -118,145 +150,201 @@ class ClockSampler:
 # ------------------------------------------------------------------ inputs
 
 
-def make_graph(device: int):
+def product_pairs(cfg: str):
+    """The config's pairs from the library's host generators (the GPU arm)."""
     from paper_1706_05151_b200 import trigraph as T
 
-    t0 = time.time()
-    pairs = T.gen_pa(N_NODES, PA_D, SEED)
-    t1 = time.time()
-    g = T.build_graph(pairs, N_NODES, device=device)
-    t2 = time.time()
-    log(f"[bench] gen_pa {t1 - t0:.1f}s, device build_graph {t2 - t1:.2f}s, "
-        f"n={g.num_nodes()} m={g.num_edges()}")
-    return g, pairs
+    kind, p, _ = CONFIGS[cfg]
+    if kind == "pa":
+        return T.gen_pa(p["n"], p["d"], p["seed"]), p["n"]
+    if kind == "gnm":
+        return T.gen_gnm(p["n"], p["m"], p["seed"]), p["n"]
+    if kind == "rmat":
+        return T.gen_rmat(p["scale"], p["ef"], p["a"], p["b"], p["c"], p["seed"]), 1 << p["scale"]
+    if kind == "ws":
+        return T.gen_ws(p["n"], p["k"], p["beta"], p["seed"]), p["n"]
+    raise ValueError(kind)
 
 
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(p) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """Per-launch DRAM bytes of the intersection pass from the committed
-    ncu --set full capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_intersect.json")
+def profile_traffic(cfg: str):
+    """(bytes per intersection pass, source) from the committed ncu --set
+    full capture of this config (dram__bytes_read.sum + write.sum), or
+    (None, reason)."""
+    rel = TRAFFIC_PROFILES.get(cfg)
+    if not rel:
+        return None, f"no ncu capture committed for {cfg}"
     try:
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_pass")
+        with open(os.path.join(ROOT, rel)) as f:
+            return json.load(f).get("dram_bytes_per_pass"), rel + " (ncu --set full, per pass)"
     except Exception:
-        return None
+        return None, f"{rel} missing"
 
 
 # ------------------------------------------------------------------ CPU legs
 
 
-def ref_setup(pairs):
-    """Reference Graph from the oracle's CSR build (input prep, untimed),
-    then the reference's compute_order + effective_adjacency (untimed)."""
+class CpuBaseline:
+    """The reference's own counting code on the host cores (oracle/_ref),
+    over the oracle-built EffectiveAdjacency of the config's graph."""
+
+    def __init__(self, pairs_buf, E: int, n: int, threads: int):
+        import numpy as np
+
+        from oracle import binding as O
+
+        self.O, self.np = O, np
+        if not O.ref_available():
+            raise RuntimeError("oracle/_ref not built (make -C oracle with /root/reference)")
+        t0 = time.time()
+        self.threads = threads
+        g = O.FullGraph(pairs_buf, E, n, threads)  # consumes pairs_buf
+        self.n, self.m = g.n, g.m
+        self.h = O.ref().ref_eff_from_arrays(g.n, C.c_void_p(g.eoff.ctypes.data),
+                                             C.c_void_p(g.eff.ctypes.data))
+        # DPD plan with p = nproc: node_costs (oracle, pinned) -> the
+        # reference's compute_boundaries (partition.hpp:116-141)
+        f = np.zeros(max(g.n, 1), dtype=np.uint64)
+        pre = np.zeros(max(g.n, 1), dtype=np.uint64)
+        O.lib().orc_node_costs(g.n, C.c_void_p(g.off.ctypes.data), C.c_void_p(g.adj.ctypes.data),
+                               C.c_void_p(g.eoff.ctypes.data), C.c_void_p(g.eff.ctypes.data),
+                               O.COSTS["DPD"], C.c_void_p(f.ctypes.data),
+                               C.c_void_p(pre.ctypes.data))
+        self.b = np.zeros(threads + 1, dtype=np.uint32)
+        O.ref().ref_compute_boundaries(C.c_void_p(f.ctypes.data), g.n, threads,
+                                       C.c_void_p(self.b.ctypes.data))
+        self.prefix = pre[: g.n]
+        del g, f
+        self.R = 256
+        self.setup_s = time.time() - t0
+        log(f"[cpu] setup {self.setup_s:.1f}s (oracle build + orientation, DPD plan p={threads})")
+
+    def close(self):
+        if self.h:
+            self.O.ref().ref_eff_free(self.h)
+            self.h = None
+
+    def ranges(self, r: int):
+        """Sub-range r of R of every core, equal DPD cost: 2p uint32."""
+        np, pre, b = self.np, self.prefix, self.b
+        out = np.zeros(2 * self.threads, dtype=np.uint32)
+        for i in range(self.threads):
+            lo, hi = int(b[i]), int(b[i + 1])
+            if hi <= lo:
+                out[2 * i] = out[2 * i + 1] = lo
+                continue
+            c0 = int(pre[lo - 1]) if lo else 0
+            c1 = int(pre[hi - 1])
+            a = c0 + (c1 - c0) * r // self.R
+            z = c0 + (c1 - c0) * (r + 1) // self.R
+            s = int(np.searchsorted(pre[lo:hi], a, side="right")) + lo if r else lo
+            e = int(np.searchsorted(pre[lo:hi], z, side="right")) + lo if r + 1 < self.R else hi
+            out[2 * i], out[2 * i + 1] = s, max(s, e)
+        return out
+
+    def aop(self, r: int):
+        """One all-core sample: (count_s, build_s, edges, triangles, stored)."""
+        s = self.ranges(r % self.R)
+        tb = C.c_double()
+        e, t, st = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        dt = self.O.ref().ref_aop_threads(self.h, C.c_void_p(s.ctypes.data), self.threads,
+                                          C.byref(tb), C.byref(e), C.byref(t), C.byref(st))
+        return float(dt), tb.value, e.value, t.value, st.value
+
+    def seq(self, r: int):
+        """One 1-thread sample: (seconds, edges, triangles)."""
+        s = self.ranges(r % self.R)
+        e, t = C.c_uint64(), C.c_uint64()
+        dt = self.O.ref().ref_seq_sample(self.h, C.c_void_p(s.ctypes.data), self.threads,
+                                         C.byref(e), C.byref(t))
+        return float(dt), e.value, t.value
+
+    def calibrate(self, target_s: float):
+        """Pick R (sub-ranges per core) so one all-core sample counts for
+        ~target_s seconds."""
+        dt, _, _, _, _ = self.aop(0)
+        full = dt * self.R
+        self.R = max(1, min(1 << 16, int(round(full / max(target_s, 1e-3)))))
+        log(f"[cpu] calibration: full all-core count ~{full:.0f}s -> R={self.R}")
+
+    def report(self, samples: int = 3, seq_budget_s: float = 8.0):
+        rates = [self.aop(17 * k + 1) for k in range(samples)]
+        ct = sum(x[0] for x in rates)
+        bt = sum(x[1] for x in rates)
+        ed = sum(x[2] for x in rates)
+        st = sum(x[4] for x in rates)
+        s_t = s_e = 0
+        k = 0
+        while s_t < seq_budget_s and k < 64:
+            dt, e, _ = self.seq(31 * k + 5)
+            s_t += dt
+            s_e += e
+            k += 1
+        return {"value": ed / ct if ct > 0 else None, "unit": UNIT, "cores": self.threads,
+                "kind": "reference",
+                "sample": (f"{samples} samples x {self.threads} std::threads (p = nproc DPD "
+                           f"cores, each thread 1/{self.R} of its core's cost, rotating): "
+                           f"reference aop_count over build_overlap_partition, "
+                           f"{ed} oriented edges counted in {ct:.2f}s"),
+                "counting_s": ct, "partition_build_s": bt,
+                "partition_stored_entries": st,
+                "one_thread": {"value": s_e / s_t if s_t > 0 else None, "unit": UNIT,
+                               "cores": 1,
+                               "sample": f"count_node_iterator_n loop over {k} x {self.threads} "
+                                         f"sub-ranges ({s_e} oriented edges, {s_t:.2f}s)"},
+                "setup_s": self.setup_s}
+
+
+def oracle_pairs(cfg: str, threads: int):
     from oracle import binding as O
 
-    t0 = time.time()
-    csr = O.build_graph(pairs, N_NODES)
-    if O.ref_available():
-        R = O.RefGraph.from_csr(csr)
-        O.ref().ref_prepare(R.h)
-        kind = "reference"
-    else:
-        R, kind = None, "port"
-    log(f"[bench] CPU baseline setup ({kind}) {time.time() - t0:.1f}s")
-    return O, csr, R, kind
-
-
-def ref_sample(O, R, csr, parts, which, threads):
-    import numpy as np
-
-    if R is not None:
-        w = np.ascontiguousarray(which, dtype=np.uint64)
-        e = np.zeros(1, np.uint64)
-        t = np.zeros(1, np.uint64)
-        dt = O.ref().ref_aop_sample(R.h, parts, C.c_void_p(w.ctypes.data), len(w), threads,
-                                    C.c_void_p(e.ctypes.data), C.c_void_p(t.ctypes.data))
-        return float(dt), int(e[0]), int(t[0])
-    # oracle port (only when oracle/_ref is absent): NodeIteratorN over the
-    # apexes of the sampled DPD parts, one thread
-    eoff, eff, b = _port_state(O, csr, parts)
-    t0 = time.time()
-    edges = tris = 0
-    for i in which:
-        lo, hi = int(b[i]), int(b[i + 1])
-        tris += int(O.lib().orc_count_range(csr.n, C.c_void_p(eoff.ctypes.data),
-                                            C.c_void_p(eff.ctypes.data), lo, hi))
-        edges += int(eoff[hi] - eoff[lo])
-    return time.time() - t0, edges, tris
-
-
-_PORT = {}
-
-
-def _port_state(O, csr, parts):
-    if "eoff" not in _PORT:
-        _PORT["eoff"], _PORT["eff"] = O.effective(csr)
-        f, _ = O.node_costs(csr, "DPD")
-        _PORT["b"] = O.compute_boundaries(f, parts)
-    return _PORT["eoff"], _PORT["eff"], _PORT["b"]
-
-
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+    kind, p, _ = CONFIGS[cfg]
+    return O.gen_pairs(kind, p, threads)
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU arm
-    from paper_1706_05151_b200 import trigraph as T
-
-    pairs = T.gen_pa(N_NODES, PA_D, SEED)
-    O, csr, R, kind = ref_setup(pairs)
-    del pairs
     threads = cpu_threads()
-    parts = 256
-    budget = float(os.environ.get("TG_REF_BUDGET_S", "150"))
-    # calibrate: one batch of `threads` parts
-    order = [(k * 97) % parts for k in range(parts)]  # rotating strided sample
-    pos = 0
-
-    def take(k):
-        nonlocal pos
-        w = [order[(pos + i) % parts] for i in range(k)]
-        pos = (pos + k) % parts
-        return w
-
-    if R is None:
-        threads = 1
-    dt, e, t = ref_sample(O, R, csr, parts, take(threads), threads)  # one batch
-    steps_total = args.steps + args.warmup
-    per_step = max(1, int((budget / steps_total) / max(dt, 1e-3))) * threads
-    per_step = min(per_step, parts)
-    for _ in range(args.warmup):
-        ref_sample(O, R, csr, parts, take(per_step), threads)
-    tt = ee = 0
-    for _ in range(args.steps):
-        dt, e, t = ref_sample(O, R, csr, parts, take(per_step), threads)
-        tt += dt
-        ee += e
-    value = ee / tt if tt > 0 else 0.0
-    sample = (f"{per_step} of 256 DPD parts per step (rotating), build_overlap_partition + "
-              f"aop_count on {threads} std::threads; order+orientation precomputed untimed")
+    t0 = time.time()
+    buf, E, n = oracle_pairs(args.config, threads)
+    log(f"[ref] oracle generator {time.time() - t0:.1f}s, {E} pairs")
+    cb = CpuBaseline(buf, E, n, threads)
+    cb.calibrate(args.ref_step_s)
+    for k in range(args.warmup):
+        cb.aop(k)
+    ct = bt = 0.0
+    ed = 0
+    for k in range(args.steps):
+        dt, tb, e, _, _ = cb.aop(args.warmup + k)
+        ct += dt
+        bt += tb
+        ed += e
+    value = ed / ct if ct > 0 else 0.0
+    one = cb.report(samples=1, seq_budget_s=args.ref_seq_s)["one_thread"]
+    cb.close()
+    sample = (f"per step: {threads} std::threads, each the reference build_overlap_partition "
+              f"(timed apart: {bt:.2f}s over the run) + aop_count (the counting phase, timed) "
+              f"on 1/{cb.R} of its p = {threads} DPD core, rotating")
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1000 * tt / max(args.steps, 1),
+           "warmup": args.warmup, "ms_per_step": 1000 * ct / max(args.steps, 1),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-           "data": "synthetic (seeded gen_pa stream)", "impl": "reference",
-           "config": {"workload": WORKLOAD, "parallelism": f"cpu{threads}"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                            "sample": sample},
+           "data": "synthetic (seeded generator of the config, oracle/fullsize.c)",
+           "impl": "reference",
+           "config": {"workload": CONFIGS[args.config][2], "n": cb.n, "m": cb.m,
+                      "parallelism": f"cpu{threads}"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": sample, "partition_build_s": bt, "counting_s": ct,
+                            "one_thread": one, "setup_s": cb.setup_s},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -278,8 +366,25 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = lib()
-    g, pairs = make_graph(local)
+    t0 = time.time()
+    pairs, n0 = product_pairs(args.config)
+    E_pairs = int(pairs.shape[0])
+    t1 = time.time()
+    # build_graph on the device from device-resident pairs, timed with CUDA
+    # events (graph.hpp:58-85: radix sort + unique + offsets)
+    d_pairs = torch.from_numpy(pairs.view(np.int32)).to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eb0.record()
+    g = T.build_graph_from_pointer(d_pairs.data_ptr(), pairs.shape[0], n0, device=local)
+    eb1.record()
+    torch.cuda.synchronize()
+    build_ms = eb0.elapsed_time(eb1)
+    del d_pairs
+    torch.cuda.empty_cache()
     n, m = g.num_nodes(), g.num_edges()
+    log(f"[bench] {args.config}: host generator {t1 - t0:.1f}s, device build_graph "
+        f"{build_ms:.1f} ms, n={n} m={m}")
     W = T.ordering_cost(g)
     # a dedicated (non-default) stream shared by the library and torch, so the
     # CUDA events below bracket exactly the library's launches
@@ -288,7 +393,6 @@ def run_ours(args):
     check(L.tg_set_stream(g._h, C.c_void_p(stream.cuda_stream)))
     d_total = torch.zeros(1, dtype=torch.int64, device="cuda")
     dptr = C.c_void_p(d_total.data_ptr())
-    want = None
 
     if ws > 1:
         plan = T.compute_boundaries(g, T.CostKind.Dpd, ws).boundaries
@@ -314,8 +418,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     T_total = int(d_total.item())
     ev_mid.clear()
-    # timed region: inputs (1.7 GB CSR + 0.8 GB oriented CSR) exceed the
-    # 126 MB L2, so no explicit flush between steps
+    # timed region: the inputs (CSR + oriented CSR) exceed the 126 MB L2 for
+    # C2-C5, so no explicit flush between steps
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -367,9 +471,6 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if dist:
-            # each rank uploads 1/N of the host CSR, NCCL all-gathers the rest
-            # over NVLink, counts its AOP core; one all-reduce of T (8 bytes
-            # back to the host)
             from paper_1706_05151_b200.distributed import count_aop_from_host_csr
             cnt = count_aop_from_host_csr(n, off_p, adj_p, plan, torch.device("cuda", local))
         else:
@@ -400,51 +501,53 @@ def run_ours(args):
         d_adj.copy_(adj_p, non_blocking=True)
         torch.cuda.synchronize()
         h2d_t.append(time.perf_counter() - t0)
-    del d_off, d_adj
+    del d_off, d_adj, off_p, adj_p
     h2d_floor = min(h2d_t)
 
     if rank != 0:
         return
     # ---- roofline of the intersection pass: 4 bytes x W algorithmic elements
     peak, peak_kind = measured_peak()
-    if ws > 1:
-        w_rank = W / ws  # DPD balances W across ranks (max/mean ~1.0 at p=8)
-    else:
-        w_rank = W
+    w_rank = W / ws if ws > 1 else W  # DPD balances W across ranks
     achieved = 4.0 * w_rank / (isect_avg / 1e3) / 1e9
+    traffic, traffic_src = profile_traffic(args.config)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": profile_traffic(),
-                "kernel": "intersect pass (k_intersect_quad + k_intersect_ctaq)",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "intersect pass (k_intersect_quad + the CTA / group kernels)",
                 "algorithmic_bytes_per_pass": 4 * w_rank, "W": W,
                 "pass_ms": isect_avg, "orient_ms": orient_avg, "peak_source": peak_kind}
 
-    # ---- CPU baseline (reference on the host cores), bounded sample
+    # ---- CPU baseline (the reference's counting code on the host cores),
+    # bounded sample of the same graph
     cpu = None
     if ws == 1 and not args.no_cpu:
-        O, csr, R, kind = ref_setup(pairs)
-        threads = cpu_threads() if R is not None else 1
-        parts = 256
-        which = [(k * 97) % parts for k in range(min(parts, max(threads, args.cpu_parts)))]
-        dt, e, t = ref_sample(O, R, csr, parts, which, threads)
-        cpu = {"value": e / dt if dt > 0 else None, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"{len(which)} of 256 DPD-plan AOP parts of the same graph "
-                         f"({e} oriented edges): build_overlap_partition + aop_count on "
-                         f"{threads} std::threads, {dt:.1f}s"}
+        from oracle import binding as O
+
+        threads = cpu_threads()
+        buf = O.HostBuf.from_array(pairs)
+        del pairs
+        cb = CpuBaseline(buf, E_pairs, n0, threads)
+        cb.calibrate(args.cpu_step_s)
+        cpu = cb.report(samples=args.cpu_samples, seq_budget_s=args.cpu_seq_s)
+        cb.close()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (seeded gen_pa stream, bit-identical to the reference generator)",
-        "config": {"workload": WORKLOAD, "n": n, "m": m, "triangles": T_total,
+        "data": "synthetic (seeded generator of the config, bit-identical to the reference "
+                "gen_pa stream / the oracle's generators)",
+        "config": {"workload": CONFIGS[args.config][2], "n": n, "m": m, "triangles": T_total,
                    "parallelism": f"aop{ws}" if ws > 1 else "single",
                    "step": "orientation + intersection over the HBM-resident graph",
-                   "l2": "inputs (1.7 GB CSR, 0.8 GB oriented CSR) > 126 MB L2; no flush"},
+                   "l2": "inputs (CSR + oriented CSR) > 126 MB L2; no flush"},
         "intersections_per_s": value,
         # oriented edges / intersection time (kernel only, the
         # orientation excluded), slowest rank at N > 1
         "kernel_only": {"edges_per_s": m / (isect_max / 1e3), "intersect_ms": isect_max,
                         "orient_ms": orient_avg},
-        "elements_per_s": W / (ms_per_step / 1e3) / ws * ws,
+        "elements_per_s": W / (ms_per_step / 1e3),
+        "build_graph": {"ms": build_ms, "pairs": E_pairs,
+                        "path": "device pairs -> CSR (CUB radix sort + unique), CUDA events"},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -468,13 +571,20 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-warmup", type=int, default=2)
-    ap.add_argument("--cpu-parts", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=3)
+    ap.add_argument("--cpu-step-s", type=float, default=3.0,
+                    help="all-core counting seconds per CPU-baseline sample")
+    ap.add_argument("--cpu-seq-s", type=float, default=8.0)
+    ap.add_argument("--ref-step-s", type=float, default=1.5,
+                    help="--impl reference: all-core counting seconds per step")
+    ap.add_argument("--ref-seq-s", type=float, default=8.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

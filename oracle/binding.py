@@ -67,6 +67,16 @@ def lib():
             "orc_compute_order": (i32, [u64, vp, vp, i32, u64, vp]),
             "orc_run_engine_ord": (u64, [u64, vp, vp, i32, u64, i32, vp, vp, vp, vp, vp,
                                          vp, vp, vp, u64, i32, dbl, u64, i32, u64]),
+            # fullsize.c
+            "orc_gen_pa": (u64, [u64, u64, u64, C.POINTER(vp)]),
+            "orc_gen_gnm": (u64, [u64, u64, u64, C.POINTER(vp)]),
+            "orc_gen_rmat": (u64, [C.c_uint32, u64, dbl, dbl, dbl, u64, i32, C.POINTER(vp)]),
+            "orc_gen_ws": (u64, [u64, u64, dbl, u64, i32, C.POINTER(vp)]),
+            "orc_build_graph_lean": (u64, [vp, u64, u64, i32, C.POINTER(vp), C.POINTER(vp)]),
+            "orc_effective_mt": (u64, [u64, vp, vp, vp, i32, vp, C.POINTER(vp)]),
+            "orc_tri_hash": (u64, [C.c_uint32, C.c_uint32, C.c_uint32]),
+            "orc_count_full": (u64, [u64, vp, vp, vp, u64, i32, vp, vp, vp, vp]),
+            "orc_surrogate_messages": (None, [u64, vp, vp, vp, u64, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -117,9 +127,10 @@ def ref():
             "ref_keep_entry": (i32, [dbl, u64, i32, u64, C.c_uint32, C.c_uint32]),
             "ref_per_edge_counts": (u64, [vp, vp]),
             "ref_variance_report": (None, [vp, vp, u64, dbl, vp, vp]),
-            "ref_time_sequential": (dbl, [vp, vp]),
-            "ref_prepare": (None, [vp]),
-            "ref_aop_sample": (dbl, [vp, u64, vp, u64, i32, vp, vp]),
+            "ref_eff_from_arrays": (vp, [u64, vp, vp]),
+            "ref_eff_free": (None, [vp]),
+            "ref_seq_sample": (dbl, [vp, vp, u64, vp, vp]),
+            "ref_aop_threads": (dbl, [vp, vp, u64, vp, vp, vp, vp]),
             "ref_compute_order": (None, [vp, i32, u64, vp]),
             "ref_coreness": (None, [vp, vp]),
             "ref_parse_edge_list": (u64, [C.c_char_p, u64, vp, u64, vp, vp, u64]),
@@ -558,3 +569,172 @@ def ref_random_graph(n, density, seed) -> RefGraph:
 
 def ref_fixture(name: str, *args) -> RefGraph:
     return RefGraph(getattr(ref(), "ref_" + name)(*args))
+
+
+# ---------------------------------------------------------------- full size
+# fullsize.c: the configs' generators and the memory-lean multi-threaded
+# pipeline behind the C3/C4/C5 goldens (tests/golden/make_golden_full.py).
+
+import weakref  # noqa: E402
+
+
+class HostBuf:
+    """A malloc'ed oracle buffer; freed with orc_free when dropped.  `.array`
+    is a zero-copy numpy view (keep the HostBuf alive while it is used)."""
+
+    def __init__(self, ptr: C.c_void_p, ctype, count: int):
+        self.ptr = ptr
+        self.count = count
+        self.array = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), (max(count, 1),))[:count]
+        self._fin = weakref.finalize(self, lib().orc_free, ptr)
+
+    @classmethod
+    def from_array(cls, a: np.ndarray, ctype=C.c_uint32) -> "HostBuf":
+        """malloc'ed copy of a numpy array (for the consuming C calls)."""
+        a = np.ascontiguousarray(a)
+        libc = C.CDLL(None)
+        libc.malloc.restype = C.c_void_p
+        libc.malloc.argtypes = [C.c_size_t]
+        ptr = C.c_void_p(libc.malloc(max(a.nbytes, 1)))
+        if not ptr.value:
+            raise MemoryError("malloc failed")
+        C.memmove(ptr, a.ctypes.data, a.nbytes)
+        return cls(ptr, ctype, a.nbytes // C.sizeof(ctype))
+
+    def release(self) -> C.c_void_p:
+        """Hand the pointer to a consuming C call (no free here)."""
+        self._fin.detach()
+        self.array = None
+        return self.ptr
+
+
+CONFIGS = {  # BASELINE.json configs (seeds recorded with the goldens)
+    "C1": ("gnm", dict(n=100_000, m=1_000_000, seed=1)),
+    "C2": ("pa", dict(n=10_000_000, d=40, seed=7)),
+    "C3": ("rmat", dict(scale=24, ef=16, a=0.57, b=0.19, c=0.19, seed=1)),
+    "C4": ("ws", dict(n=50_000_000, k=20, beta=0.1, seed=1)),
+    "C5": ("pa", dict(n=100_000_000, d=40, seed=7)),
+}
+
+
+def threads_default() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def gen_pairs(kind: str, p: dict, threads: int = 0):
+    """The config generators (fullsize.c).  Returns (HostBuf of 2E uint32, E, n)."""
+    L, t = lib(), threads or threads_default()
+    pp = C.c_void_p()
+    if kind == "pa":
+        E, n = L.orc_gen_pa(p["n"], p["d"], p["seed"], C.byref(pp)), p["n"]
+    elif kind == "gnm":
+        E, n = L.orc_gen_gnm(p["n"], p["m"], p["seed"], C.byref(pp)), p["n"]
+    elif kind == "rmat":
+        E = L.orc_gen_rmat(p["scale"], p["ef"], p.get("a", 0.57), p.get("b", 0.19),
+                           p.get("c", 0.19), p["seed"], t, C.byref(pp))
+        n = 1 << p["scale"]
+    elif kind == "ws":
+        E, n = L.orc_gen_ws(p["n"], p["k"], p["beta"], p["seed"], t, C.byref(pp)), p["n"]
+    else:
+        raise ValueError(kind)
+    if E == 2**64 - 1:
+        raise ValueError(f"bad generator arguments {kind} {p}")
+    return HostBuf(pp, C.c_uint32, 2 * E), int(E), int(n)
+
+
+class FullGraph:
+    """Graph + ByDegree EffectiveAdjacency built by the full-size oracle."""
+
+    def __init__(self, pairs: HostBuf, E: int, n_override: int, threads: int = 0):
+        L, t = lib(), threads or threads_default()
+        self.threads = t
+        po, pa = C.c_void_p(), C.c_void_p()
+        n = L.orc_build_graph_lean(pairs.release(), E, n_override, t, C.byref(po), C.byref(pa))
+        self.n = int(n)
+        self._off = HostBuf(po, C.c_uint64, self.n + 1)
+        self.off = self._off.array
+        self._adj = HostBuf(pa, C.c_uint32, int(self.off[-1]))
+        self.adj = self._adj.array
+        self.rank = np.zeros(max(self.n, 1), dtype=U32)
+        L.orc_degree_rank(self.n, _ptr(self.off), _ptr(self.rank))
+        self.eoff = np.zeros(self.n + 1, dtype=U64)
+        pe = C.c_void_p()
+        m = L.orc_effective_mt(self.n, _ptr(self.off), _ptr(self.adj), _ptr(self.rank), t,
+                               _ptr(self.eoff), C.byref(pe))
+        self._eff = HostBuf(pe, C.c_uint32, int(m))
+        self.eff = self._eff.array
+
+    @property
+    def m(self) -> int:
+        return int(self.off[-1]) // 2
+
+    def csr(self) -> CSR:
+        return CSR(self.n, self.off, self.adj)
+
+    def ordering_cost(self) -> int:
+        """sequential.hpp:95-104: sum_v d_v * h_v."""
+        d = np.diff(self.off)
+        h = np.diff(self.eoff)
+        return int((d * h).sum(dtype=U64))
+
+    def dpd_boundaries(self, p: int) -> np.ndarray:
+        """compute_boundaries(node_costs(DPD), p) (partition.hpp:60-69, 116-141)."""
+        f = np.zeros(max(self.n, 1), dtype=U64)
+        pre = np.zeros(max(self.n, 1), dtype=U64)
+        lib().orc_node_costs(self.n, _ptr(self.off), _ptr(self.adj), _ptr(self.eoff),
+                             _ptr(self.eff), COSTS["DPD"], _ptr(f), _ptr(pre))
+        b = np.zeros(p + 1, dtype=U32)
+        lib().orc_compute_boundaries(_ptr(pre), self.n, p, _ptr(b))
+        return b
+
+    def count(self, boundaries=None, tally=False, digest=False):
+        """count_node_iterator_n on all threads.  Returns dict(total, tally,
+        apex (AOP per-rank T), mid (surrogate per-rank T), digest)."""
+        p = 0 if boundaries is None else len(boundaries) - 1
+        b = None if boundaries is None else np.ascontiguousarray(boundaries, dtype=U32)
+        tv = np.zeros(max(self.n, 1), dtype=U64) if tally else None
+        apex = np.zeros(max(p, 1), dtype=U64) if p else None
+        mid = np.zeros(max(p, 1), dtype=U64) if p else None
+        dg = np.zeros(2, dtype=U64) if digest else None
+        total = lib().orc_count_full(self.n, _ptr(self.eoff), _ptr(self.eff), _ptr(b), p,
+                                     self.threads, _ptr(tv), _ptr(apex), _ptr(mid), _ptr(dg))
+        return {"total": int(total), "tally": None if tv is None else tv[: self.n],
+                "apex": None if apex is None else apex[:p].tolist(),
+                "mid": None if mid is None else mid[:p].tolist(),
+                "digest": None if dg is None else [int(x) for x in dg]}
+
+    def surrogate_messages(self, boundaries):
+        b = np.ascontiguousarray(boundaries, dtype=U32)
+        p = len(b) - 1
+        sent = np.zeros(p, dtype=U64)
+        recv = np.zeros(p, dtype=U64)
+        lib().orc_surrogate_messages(self.n, _ptr(self.eoff), _ptr(self.eff), _ptr(b), p,
+                                     _ptr(sent), _ptr(recv))
+        return sent.tolist(), recv.tolist()
+
+    def clustering(self, tally) -> np.ndarray:
+        c = np.zeros(max(self.n, 1), dtype=F64)
+        lib().orc_cc(self.n, _ptr(self.off), _ptr(tally), _ptr(c))
+        return c[: self.n]
+
+
+def tri_digest_np(tri) -> list:
+    """The listing digest of oracle.h orc_tri_hash over an (T, 3) array of
+    normalised triples (ascending within each row), numpy (wrapping uint64)."""
+    t = np.asarray(tri, dtype=U64).reshape(-1, 3)
+
+    def mix(x):
+        x = x + U64(0x9E3779B97F4A7C15)
+        x ^= x >> U64(30)
+        x *= U64(0xBF58476D1CE4E5B9)
+        x ^= x >> U64(27)
+        x *= U64(0x94D049BB133111EB)
+        x ^= x >> U64(31)
+        return x
+
+    with np.errstate(over="ignore"):
+        h = mix(mix(mix(t[:, 0]) ^ t[:, 1]) ^ t[:, 2])
+        return [int(h.sum(dtype=U64)), int(mix(h).sum(dtype=U64))]

@@ -157,6 +157,45 @@ typedef struct { uint64_t mt[312]; int mti; } orc_mt64;
 void orc_mt64_seed(orc_mt64* s, uint64_t seed);
 uint64_t orc_mt64_next(orc_mt64* s);
 
+
+/* ---- full-size oracle (fullsize.c): the configs' generators and the
+ * memory-lean multi-threaded pipeline used for the C3/C4/C5 goldens ---- */
+
+/* io.hpp:129-162 gen_pa; harness G(n,m) / R-MAT / Watts-Strogatz (the
+ * workload definitions of configs 1, 3, 4).  Return the pair count
+ * (*pairs_out malloc'ed, E interleaved pairs) or UINT64_MAX on bad args. */
+uint64_t orc_gen_pa(uint64_t n, uint64_t d, uint64_t seed, uint32_t** pairs_out);
+uint64_t orc_gen_gnm(uint64_t n, uint64_t m, uint64_t seed, uint32_t** pairs_out);
+uint64_t orc_gen_rmat(uint32_t scale, uint64_t edge_factor, double a, double b, double c,
+                      uint64_t seed, int threads, uint32_t** pairs_out);
+uint64_t orc_gen_ws(uint64_t n, uint64_t k, double beta, uint64_t seed, int threads,
+                    uint32_t** pairs_out);
+
+/* graph.hpp:58-85 build_graph; CONSUMES pairs (freed). Returns n. */
+uint64_t orc_build_graph_lean(uint32_t* pairs, uint64_t E, uint64_t n_override, int threads,
+                              uint64_t** off_out, uint32_t** adj_out);
+
+/* effective.hpp:37-52 on `threads` threads; eoff (n+1) caller-allocated. */
+uint64_t orc_effective_mt(uint64_t n, const uint64_t* off, const uint32_t* adj,
+                          const uint32_t* rank, int threads, uint64_t* eoff, uint32_t** eff_out);
+
+/* Digest term of one normalised triple a < b < c (ListSink order,
+ * sequential.hpp:39-44): mix(mix(mix(a) ^ b) ^ c), mix = SplitMix64
+ * finaliser (sparsify.hpp:37-45).  A listing's digest is
+ * (sum h, sum mix(h)) mod 2^64. */
+uint64_t orc_tri_hash(uint32_t a, uint32_t b, uint32_t c);
+
+/* count_node_iterator_n on `threads` threads; optional tally[n] (T_v),
+ * apex_tri[p] / mid_tri[p] (triangles by owner of apex / middle vertex under
+ * plan b: AOP / ANOP-surrogate per-rank counts), digest2[2] (listing). */
+uint64_t orc_count_full(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
+                        const uint32_t* b, uint64_t p, int threads, uint64_t* tally,
+                        uint64_t* apex_tri, uint64_t* mid_tri, uint64_t* digest2);
+
+/* engines.hpp:173-187 surrogate NeighborList messages per rank. */
+void orc_surrogate_messages(uint64_t n, const uint64_t* eoff, const uint32_t* eff,
+                            const uint32_t* b, uint64_t p, uint64_t* sent, uint64_t* recv);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,6 @@ struct RefGraph {
   Graph g;
   std::optional<OrderRank> order;
   std::optional<EffectiveAdjacency> eff;
-  std::optional<PartitionPlan> plan;  // cached DPD plan for the AOP sample
 
   const EffectiveAdjacency& effective() {
     if (!eff) {
@@ -398,57 +397,99 @@ int ref_clustering(void* h, int engine, uint64_t p, int cost, uint64_t* tally, d
 }
 
 // ---- CPU baseline legs (bench.py cpu_baseline / --impl reference) -------
+//
+// (i) one thread, count_node_iterator_n's loop; (ii) all host
+// cores, the reference AOP through its public API with p = nproc, partition
+// building and counting timed separately.  The EffectiveAdjacency is built
+// once from the oracle's arrays (pinned bit-exact against
+// effective_adjacency, tests/test_oracle_full.py) -- setup, untimed.
 
-// Full single-thread reference pipeline: compute_order + effective_adjacency
-// + count_node_iterator_n.  Returns seconds; *total = T.
-double ref_time_sequential(void* h, uint64_t* total) {
-  auto* r = static_cast<RefGraph*>(h);
+// EffectiveAdjacency(offsets, eff) (effective.hpp:18-20), copied in.
+void* ref_eff_from_arrays(uint64_t n, const uint64_t* eoff, const uint32_t* eff) {
+  std::vector<std::size_t> o(eoff, eoff + n + 1);
+  std::vector<NodeId> e(eff, eff + eoff[n]);
+  return new EffectiveAdjacency(std::move(o), std::move(e));
+}
+void ref_eff_free(void* h) { delete static_cast<EffectiveAdjacency*>(h); }
+
+// (i) sequential.hpp:74-91 count_node_iterator_n over the apexes of `nr`
+// ID ranges [r[2k], r[2k+1]) on the calling thread, with the reference's
+// intersect_visit (intersect.hpp:15-33) and NullSink.  Returns seconds.
+double ref_seq_sample(void* h, const uint32_t* r, uint64_t nr, uint64_t* edges, uint64_t* tris) {
+  const auto& eff = *static_cast<const EffectiveAdjacency*>(h);
+  uint64_t total = 0, e = 0;
+  NullSink sink;
   double t0 = now_s();
-  auto ord = compute_order(r->g, OrderKind::by_degree());
-  auto eff = effective_adjacency(r->g, ord);
-  *total = count_node_iterator_n(eff);
-  return now_s() - t0;
+  for (uint64_t k = 0; k < nr; ++k)
+    for (NodeId v = r[2 * k]; v < r[2 * k + 1]; ++v) {
+      auto nv = eff.eff(v);
+      e += nv.size();
+      for (NodeId u : nv)
+        intersect_visit(nv, eff.eff(u), [&](NodeId w) {
+          ++total;
+          sink(v, u, w);
+        });
+    }
+  double dt = now_s() - t0;
+  *edges = e;
+  *tris = total;
+  return dt;
 }
 
-// Precomputes order + effective adjacency (untimed setup for the AOP sample).
-void ref_prepare(void* h) { static_cast<RefGraph*>(h)->effective(); }
-
-// Reference AOP rank bodies on host threads: the DPD prefix-sum plan for
-// `parts` ranks (partition.hpp:116-141), then for each rank id in `which`
-// build_overlap_partition (partition.hpp:171-206) + aop_count
-// (engines.hpp:38-54) on a pool of `threads` std::threads.  Reports the
-// oriented edges (sum of effdeg over the sampled cores), triangles, and the
-// wall time of the parallel region.
-double ref_aop_sample(void* h, uint64_t parts, const uint64_t* which, uint64_t nwhich,
-                      int threads, uint64_t* edges, uint64_t* tris) {
-  auto* r = static_cast<RefGraph*>(h);
-  const auto& eff = r->effective();
-  if (!r->plan || r->plan->ranks() != parts)
-    r->plan = compute_boundaries(node_costs(r->g, eff, CostKind::Dpd), parts);
-  const PartitionPlan& plan = *r->plan;
-  std::atomic<uint64_t> next{0}, e_acc{0}, t_acc{0};
-  double t0 = now_s();
+// (ii) The reference AOP (engines.hpp:38-54 over partition.hpp:171-206) on
+// one std::thread per sampled core.  `s` holds p sub-ranges [s[2i], s[2i+1])
+// of the p = nproc cores of the DPD plan; they become the odd parts of a
+// PartitionPlan (partition.hpp:95-110) whose boundaries are {0, s_i, e_i, n}.
+// Phase 1 (timed: t_build): every thread runs build_overlap_partition for
+// its sub-core; barrier; phase 2 (timed, the return value): aop_count.
+// Reports sampled oriented edges, triangles and Σ stored_entries.
+double ref_aop_threads(void* h, const uint32_t* s, uint64_t p, double* t_build,
+                       uint64_t* edges, uint64_t* tris, uint64_t* stored) {
+  const auto& eff = *static_cast<const EffectiveAdjacency*>(h);
+  const NodeId n = static_cast<NodeId>(eff.num_nodes());
+  PartitionPlan plan;
+  plan.boundaries.push_back(0);
+  std::vector<std::size_t> part_of(p, SIZE_MAX);
+  for (uint64_t i = 0; i < p; ++i) {
+    if (s[2 * i] >= s[2 * i + 1]) continue;
+    if (plan.boundaries.back() != s[2 * i]) plan.boundaries.push_back(s[2 * i]);
+    part_of[i] = plan.boundaries.size() - 1;
+    plan.boundaries.push_back(s[2 * i + 1]);
+  }
+  if (plan.boundaries.back() != n) plan.boundaries.push_back(n);
+  Graph g;  // build_overlap_partition ignores g (partition.hpp:174)
+  std::vector<OverlapPartition> parts(p);
+  std::vector<uint64_t> tt(p, 0), ee(p, 0);
+  std::atomic<uint64_t> built{0};
+  std::atomic<bool> go{false};
+  double tb0 = now_s(), tb1 = 0;
   std::vector<std::thread> pool;
-  for (int t = 0; t < threads; ++t)
-    pool.emplace_back([&] {
-      for (;;) {
-        uint64_t k = next.fetch_add(1);
-        if (k >= nwhich) break;
-        uint64_t i = which[k];
-        auto part = build_overlap_partition(r->g, eff, plan, i);
-        NullSink sink;
-        uint64_t tt = aop_count(part, sink);
-        uint64_t ee = 0;
-        for (NodeId v = part.core_begin; v < part.core_end; ++v) ee += eff.effdeg(v);
-        e_acc += ee;
-        t_acc += tt;
+  for (uint64_t i = 0; i < p; ++i)
+    pool.emplace_back([&, i] {
+      if (part_of[i] != SIZE_MAX) parts[i] = build_overlap_partition(g, eff, plan, part_of[i]);
+      if (built.fetch_add(1) + 1 == p) {  // last builder starts the count phase
+        tb1 = now_s();
+        go.store(true);
       }
+      while (!go.load()) std::this_thread::yield();
+      if (part_of[i] == SIZE_MAX) return;
+      NullSink sink;
+      tt[i] = aop_count(parts[i], sink);
+      for (NodeId v = parts[i].core_begin; v < parts[i].core_end; ++v) ee[i] += eff.effdeg(v);
     });
   for (auto& th : pool) th.join();
-  double dt = now_s() - t0;
-  *edges = e_acc.load();
-  *tris = t_acc.load();
-  return dt;
+  double tc1 = now_s();
+  *t_build = tb1 - tb0;
+  uint64_t e = 0, t = 0, st = 0;
+  for (uint64_t i = 0; i < p; ++i) {
+    e += ee[i];
+    t += tt[i];
+    st += parts[i].stored_entries();
+  }
+  *edges = e;
+  *tris = t;
+  *stored = st;
+  return tc1 - tb1;
 }
 
 }  // extern "C"

@@ -185,14 +185,17 @@ k_intersect_quad(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
           for (int q = 0; q < kQUnroll; ++q) {
             const uint32_t base = base0 + 32 * q;
             const uint32_t word = Tbl[(base - w0) >> 5];
-            const uint32_t jj = cnt + __popc(word & le_mask) - 1u;
+            // segment of this slot; lanes past S count the end marker at S
+            // (jj = nseg), so they are clamped to the last segment and below
+            // re-read its last quad (qs + S - 1), which is in bounds
+            const uint32_t jj = min(cnt + __popc(word & le_mask) - 1u, nseg - 1u);
             // only words inside the window: the next window's first segment start
             // (marked at word kTblWords) is counted there
             cnt += base < wend ? __popc(word) : 0u;
             jjs[q] = jj;
             const uint32_t qs = __shfl_sync(FULL, my_qs, jj);
-            // lanes past S re-read an in-bounds quad; validity is applied
-            // only on the (rare) exact path below
+            // validity (head/tail slots, lanes past S) is applied only on the
+            // (rare) exact path below
             const uint32_t idx = min(base + lane, S - 1);
             r[q] = ldg_stream4(Q4 + (qs + idx));
           }

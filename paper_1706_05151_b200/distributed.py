@@ -162,9 +162,9 @@ class CudaRankBackend(RankBackend):
 
 def _all_to_allv(t: torch.Tensor, send_counts: List[int], recv_counts: List[int],
                  group=None) -> torch.Tensor:
+    # always entered: all_to_all_single is a collective, and a rank with no
+    # traffic of its own must still pair with its peers (zero splits are legal)
     out = torch.empty(sum(recv_counts), dtype=t.dtype, device=t.device)
-    if sum(send_counts) == 0 and sum(recv_counts) == 0:
-        return out
     dist.all_to_all_single(out, t, output_split_sizes=recv_counts,
                            input_split_sizes=send_counts, group=group)
     return out

@@ -2,7 +2,9 @@
 """Full-size check of a large config (default C5 = gen_pa(1e8, 40, seed 7),
 ~2e9 edges) on one B200: count, engine agreement, timing, and an oracle
 spot-check of per-rank AOP counts (apex ranges of a 4096-part DPD plan,
-counted on the host by the C restatement over the same oriented CSR).
+counted on the host by the C restatement over the oracle's own graph and
+orientation, built from the same pairs).  The full-size goldens are in
+tests/golden/reference_full.json (tests/test_gpu_full.py).
 
     python tools/check_large.py [--n 100000000] [--parts 4096] [--spot 6]
 """
@@ -39,6 +41,9 @@ def main():
     rec["gen_s"] = round(time.time() - t0, 1)
     t0 = time.time()
     g = T.build_graph(pairs, a.n)
+    # the oracle's own graph + orientation from the same pairs (never from
+    # device arrays) for the spot check below
+    og = None if a.quick else O.FullGraph(O.HostBuf.from_array(pairs), pairs.shape[0], a.n)
     del pairs
     torch.cuda.synchronize()
     rec["build_s"] = round(time.time() - t0, 2)
@@ -79,13 +84,12 @@ def main():
         assert sum(r.triangles for r in rep.per_rank) == T_
     # oracle spot-check: per-rank AOP counts of a fine plan
     rep = T.run_engine(g, T.EngineConfig(engine=T.EngineKind.Aop, ranks=a.parts))
-    eff = T.effective_adjacency(g)
     rng = np.random.default_rng(1)
     spots = []
     for i in sorted(rng.choice(a.parts, a.spot, replace=False)):
         lo, hi = int(rep.boundaries[i]), int(rep.boundaries[i + 1])
-        want = O.lib().orc_count_range(rec["n"], C.c_void_p(eff.offsets.ctypes.data),
-                                       C.c_void_p(eff.entries.ctypes.data), lo, hi)
+        want = O.lib().orc_count_range(og.n, C.c_void_p(og.eoff.ctypes.data),
+                                       C.c_void_p(og.eff.ctypes.data), lo, hi)
         spots.append([int(i), lo, hi, int(rep.per_rank[i].triangles), int(want)])
         assert rep.per_rank[i].triangles == want, spots[-1]
     rec["oracle_spots"] = spots
