@@ -66,7 +66,8 @@ typedef enum {
   TG_ORDER_BY_ID = 0,
   TG_ORDER_BY_DEGREE = 1, /* the reference default and the hot path */
   TG_ORDER_BY_RANDOM = 2, /* seeded Fisher-Yates, mt19937_64 */
-  TG_ORDER_BY_CORENESS = 3
+  TG_ORDER_BY_CORENESS = 3,
+  TG_ORDER_RANK = 16 /* a caller-supplied OrderRank (tg_set_order_rank) */
 } tg_order;
 
 /* engines.hpp:270-280 EngineConfig.  ExecMode has no meaning on the device
@@ -157,6 +158,12 @@ tg_status tg_set_stream(tg_graph* g, void* stream);
  * Fisher-Yates on the host).  Drops the cached oriented CSR when the order
  * changes.  TG_ERR_INVALID_ARGUMENT for an unknown kind. */
 tg_status tg_set_order(tg_graph* g, int32_t kind, uint64_t seed);
+/* Orient by a caller's OrderRank (order.hpp:31-35): precedes(u, v) iff
+ * rank[u] < rank[v]; rank = n entries (host or device), a permutation of
+ * [0, n) (checked for host input; TG_ERR_INVALID_ARGUMENT otherwise).  The
+ * two-argument effective_adjacency(g, order) (effective.hpp:37-52) is
+ * tg_set_order_rank + tg_effective_adjacency. */
+tg_status tg_set_order_rank(tg_graph* g, const uint32_t* rank);
 /* coreness(g) (order.hpp:39-83): core numbers, n entries (host). */
 tg_status tg_coreness(tg_graph* g, uint64_t* core);
 /* compute_order(g, <current order>).rank (n entries). */
@@ -166,6 +173,27 @@ tg_status tg_compute_order(tg_graph* g, uint32_t* rank);
 tg_status tg_effective_adjacency(tg_graph* g, uint64_t* offsets, uint32_t* eff);
 /* ordering_cost(g, <current order>) (sequential.hpp:95-104) = W. */
 tg_status tg_ordering_cost(tg_graph* g, uint64_t* cost);
+
+/* ---- EffectiveAdjacency as a value (effective.hpp:17-35) ---- */
+
+/* EffectiveAdjacency(offsets, eff) (effective.hpp:18-20) adopted on
+ * `device`: offsets n+1, entries offsets[n]; each list ID-sorted, ids < n
+ * (checked for host input).  The handle owns the device copy. */
+typedef struct tg_eff tg_eff;
+tg_status tg_eff_from_csr(int device, uint64_t n, const uint64_t* offsets,
+                          const uint32_t* entries, tg_eff** out);
+tg_status tg_eff_free(tg_eff* e);
+/* count_node_iterator_n(eff, sink) (sequential.hpp:74-91) over an adopted
+ * EffectiveAdjacency.  total: the count.  tally (n, host or device, may be
+ * NULL): NodeTallySink counts (sequential.hpp:24-33).  triples (3*capacity
+ * uint32, host or device, may be NULL): every triangle once, either
+ * normalised ascending (raw = 0, ListSink, sequential.hpp:36-46) or as the
+ * sink call's (v, u, w) -- apex v, u in N_v, w in N_v cap N_u (raw = 1) --
+ * in unspecified order; sorting raw triples by (v, u, w) gives the
+ * reference's emission order.  *num_triangles = total; TG_ERR_CAPACITY when
+ * capacity < total. */
+tg_status tg_eff_count(tg_eff* e, uint64_t* total, uint64_t* tally, uint32_t* triples,
+                       uint64_t capacity, int32_t raw, uint64_t* num_triangles);
 
 /* ---- partitioning (partition.hpp:45-141) ---- */
 

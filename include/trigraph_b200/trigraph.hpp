@@ -9,9 +9,11 @@
 // Names and argument meaning follow the reference (file:line cited per
 // symbol).  Differences: Graph lives on a CUDA device;
 // ExecMode is accepted and ignored;
-// RankStats::realized_cost is algorithmic work, not merge comparisons;
-// effective adjacency / order helpers take the Graph (the device keeps the
-// oriented CSR cached) instead of an EffectiveAdjacency / OrderRank.
+// RankStats::realized_cost is algorithmic work, not merge comparisons.
+// Besides the reference's signatures (effective_adjacency(g, OrderRank),
+// count_node_iterator_n(eff, sink), count_node_iterator_pp(g, OrderRank)),
+// the order-dependent helpers also take the Graph plus an OrderKind (the
+// device keeps the oriented CSR cached).
 #ifndef TRIGRAPH_B200_TRIGRAPH_HPP
 #define TRIGRAPH_B200_TRIGRAPH_HPP
 
@@ -19,8 +21,12 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <algorithm>
 #include <map>
+#include <memory>
 #include <optional>
+#include <span>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -65,15 +71,19 @@ class Graph {
         int device = 0) {
     std::vector<std::uint64_t> off(offsets.begin(), offsets.end());
     detail::check(tg_graph_from_csr(device, n, off.data(), adj.empty() ? nullptr : adj.data(), &h_));
+    device_ = device;
   }
-  explicit Graph(tg_graph* h) : h_(h) {}
+  explicit Graph(tg_graph* h, int device = 0) : h_(h), device_(device) {}
   Graph(const Graph&) = delete;
   Graph& operator=(const Graph&) = delete;
-  Graph(Graph&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Graph(Graph&& o) noexcept
+      : h_(std::exchange(o.h_, nullptr)), device_(o.device_), host_(std::move(o.host_)) {}
   Graph& operator=(Graph&& o) noexcept {
     if (this != &o) {
       if (h_) tg_graph_free(h_);
       h_ = std::exchange(o.h_, nullptr);
+      device_ = o.device_;
+      host_ = std::move(o.host_);
     }
     return *this;
   }
@@ -84,6 +94,7 @@ class Graph {
   std::size_t num_nodes() const { return info().first; }   // graph.hpp:25
   std::size_t num_edges() const { return info().second; }  // graph.hpp:26
   tg_graph* handle() const { return h_; }
+  int device() const { return device_; }
 
   /// Host copy of the CSR (offsets n+1, adjacency 2m).
   std::pair<std::vector<std::uint64_t>, std::vector<NodeId>> csr() const {
@@ -94,13 +105,43 @@ class Graph {
     return {std::move(off), std::move(adj)};
   }
 
+  /// graph.hpp:28-46 accessors, served from a host copy of the (immutable)
+  /// CSR downloaded on first use.
+  std::size_t degree(NodeId v) const {
+    const auto& c = host();
+    return c.first[v + 1] - c.first[v];
+  }
+  std::span<const NodeId> neighbors(NodeId v) const {
+    const auto& c = host();
+    return {c.second.data() + c.first[v], c.second.data() + c.first[v + 1]};
+  }
+  bool has_edge(NodeId u, NodeId v) const {
+    auto nb = neighbors(u);
+    return std::binary_search(nb.begin(), nb.end(), v);
+  }
+  std::vector<std::pair<NodeId, NodeId>> edges() const {  // u < v, u then v ascending
+    std::vector<std::pair<NodeId, NodeId>> out;
+    const auto& c = host();
+    for (NodeId u = 0; u + 1 < c.first.size(); ++u)
+      for (std::uint64_t i = c.first[u]; i < c.first[u + 1]; ++i)
+        if (u < c.second[i]) out.emplace_back(u, c.second[i]);
+    return out;
+  }
+
  private:
   std::pair<std::size_t, std::size_t> info() const {
     std::uint64_t n = 0, m = 0;
     detail::check(tg_graph_info(h_, &n, &m));
     return {n, m};
   }
+  const std::pair<std::vector<std::uint64_t>, std::vector<NodeId>>& host() const {
+    if (!host_)
+      host_ = std::make_shared<std::pair<std::vector<std::uint64_t>, std::vector<NodeId>>>(csr());
+    return *host_;
+  }
   tg_graph* h_ = nullptr;
+  int device_ = 0;
+  mutable std::shared_ptr<std::pair<std::vector<std::uint64_t>, std::vector<NodeId>>> host_;
 };
 
 /// graph.hpp:58-85 build_graph, on the device.
@@ -114,7 +155,7 @@ inline Graph build_graph(const std::vector<std::pair<NodeId, NodeId>>& edge_pair
   tg_graph* h = nullptr;
   detail::check(tg_graph_from_edges(device, flat.empty() ? nullptr : flat.data(), edge_pairs.size(),
                                     n_override, &h));
-  return Graph(h);
+  return Graph(h, device);
 }
 
 /// order.hpp:17-28.
@@ -158,25 +199,139 @@ inline std::vector<std::size_t> coreness(const Graph& g) {
   return std::vector<std::size_t>(c.begin(), c.end());
 }
 
-/// effective.hpp:17-52 under `order` (default ByDegree).
-struct EffectiveAdjacency {
-  std::vector<std::uint64_t> offsets{0};
-  std::vector<NodeId> entries;
+namespace detail {
+// The graph orients by a caller's OrderRank from here on (tg_set_order_rank).
+inline void use_order(const Graph& g, const OrderRank& order) {
+  if (order.rank.size() != g.num_nodes())
+    throw std::invalid_argument("OrderRank: rank must have num_nodes() entries");
+  check(tg_set_order_rank(g.handle(), order.rank.empty() ? nullptr : order.rank.data()));
+}
+}  // namespace detail
+
+/// effective.hpp:17-35.  N_v (ID-sorted) for every v, as host vectors; the
+/// first count_node_iterator_n over it adopts a copy on the device
+/// (tg_eff_from_csr) that later counts reuse.
+class EffectiveAdjacency {
+ public:
+  EffectiveAdjacency() = default;
+  /// EffectiveAdjacency(offsets, eff) (effective.hpp:18-20).
+  EffectiveAdjacency(std::vector<std::size_t> offsets_, std::vector<NodeId> eff_, int device = 0)
+      : offsets(offsets_.begin(), offsets_.end()), entries(std::move(eff_)), device_(device) {}
+
   std::size_t num_nodes() const { return offsets.size() - 1; }
   std::size_t total_entries() const { return entries.size(); }
+  std::span<const NodeId> eff(NodeId v) const {
+    return {entries.data() + offsets[v], entries.data() + offsets[v + 1]};
+  }
   std::size_t effdeg(NodeId v) const { return offsets[v + 1] - offsets[v]; }
+
+  std::vector<std::uint64_t> offsets{0};
+  std::vector<NodeId> entries;
+
+  /// The device copy (created on first use).
+  tg_eff* handle() const {
+    if (!dev_) {
+      tg_eff* h = nullptr;
+      detail::check(tg_eff_from_csr(device_, num_nodes(), offsets.data(),
+                                    entries.empty() ? nullptr : entries.data(), &h));
+      dev_ = std::shared_ptr<tg_eff>(h, [](tg_eff* p) { tg_eff_free(p); });
+    }
+    return dev_.get();
+  }
+
+ private:
+  friend EffectiveAdjacency effective_adjacency_from(const Graph&);
+  int device_ = 0;
+  mutable std::shared_ptr<tg_eff> dev_;
 };
-inline EffectiveAdjacency effective_adjacency(const Graph& g,
-                                              OrderKind order = OrderKind::by_degree()) {
-  detail::use_order(g, order);
+
+/// The graph's current orientation, downloaded (compact, ID-sorted lists).
+inline EffectiveAdjacency effective_adjacency_from(const Graph& g) {
   EffectiveAdjacency e;
   e.offsets.resize(g.num_nodes() + 1);
   e.entries.resize(g.num_edges());
   detail::check(tg_effective_adjacency(g.handle(), e.offsets.data(), e.entries.data()));
+  e.device_ = g.device();
   return e;
 }
 
-/// sequential.hpp:74-91 (count only).
+/// effective.hpp:37-52 effective_adjacency(g, order) -- the reference's
+/// signature, with the OrderRank of compute_order (or any permutation).
+inline EffectiveAdjacency effective_adjacency(const Graph& g, const OrderRank& order) {
+  detail::use_order(g, order);
+  return effective_adjacency_from(g);
+}
+/// ... and under an OrderKind (default ByDegree).
+inline EffectiveAdjacency effective_adjacency(const Graph& g,
+                                              OrderKind order = OrderKind::by_degree()) {
+  detail::use_order(g, order);
+  return effective_adjacency_from(g);
+}
+
+/// sequential.hpp:19-46 sinks.
+struct NullSink {
+  void operator()(NodeId, NodeId, NodeId) const {}
+};
+struct NodeTallySink {
+  std::vector<std::uint64_t> counts;
+  explicit NodeTallySink(std::size_t n) : counts(n, 0) {}
+  void operator()(NodeId v, NodeId u, NodeId w) {
+    ++counts[v];
+    ++counts[u];
+    ++counts[w];
+  }
+};
+struct ListSink {
+  std::vector<std::array<NodeId, 3>> triangles;
+  void operator()(NodeId v, NodeId u, NodeId w) {
+    std::array<NodeId, 3> t{v, u, w};
+    if (t[0] > t[1]) std::swap(t[0], t[1]);
+    if (t[1] > t[2]) std::swap(t[1], t[2]);
+    if (t[0] > t[1]) std::swap(t[0], t[1]);
+    triangles.push_back(t);
+  }
+};
+
+/// sequential.hpp:74-91 count_node_iterator_n(eff, sink), on the device:
+///   NullSink      -> the count;
+///   NodeTallySink -> the device TALLY path (counts added to sink.counts);
+///   ListSink      -> the device LIST path (normalised triples appended);
+///   any other callable sink(v, u, w) -> the raw (apex, middle, w) triples
+///     listed on the device, sorted by (v, u, w) and replayed on the host --
+///     the reference's emission order (v ascending, u along the ID-sorted
+///     N_v, w ascending).
+template <class Sink>
+std::uint64_t count_node_iterator_n(const EffectiveAdjacency& eff, Sink&& sink) {
+  using S = std::decay_t<Sink>;
+  tg_eff* h = eff.handle();
+  std::uint64_t t = 0, nt = 0;
+  if constexpr (std::is_same_v<S, NullSink>) {
+    detail::check(tg_eff_count(h, &t, nullptr, nullptr, 0, 0, &nt));
+  } else if constexpr (std::is_same_v<S, NodeTallySink>) {
+    std::vector<std::uint64_t> tv(eff.num_nodes());
+    detail::check(tg_eff_count(h, &t, tv.empty() ? nullptr : tv.data(), nullptr, 0, 0, &nt));
+    for (std::size_t v = 0; v < tv.size() && v < sink.counts.size(); ++v) sink.counts[v] += tv[v];
+  } else {
+    detail::check(tg_eff_count(h, &t, nullptr, nullptr, 0, 0, &nt));
+    std::vector<std::array<NodeId, 3>> tri(t);
+    constexpr int raw = std::is_same_v<S, ListSink> ? 0 : 1;
+    detail::check(tg_eff_count(h, &t, nullptr, tri.empty() ? nullptr : tri.front().data(), t,
+                               raw, &nt));
+    if constexpr (std::is_same_v<S, ListSink>) {
+      sink.triangles.insert(sink.triangles.end(), tri.begin(), tri.end());
+    } else {
+      std::sort(tri.begin(), tri.end());
+      for (const auto& x : tri) sink(x[0], x[1], x[2]);
+    }
+  }
+  return t;
+}
+inline std::uint64_t count_node_iterator_n(const EffectiveAdjacency& eff) {
+  return count_node_iterator_n(eff, NullSink{});
+}
+
+/// sequential.hpp:74-91 over effective_adjacency(g, order) (count only;
+/// the oriented CSR stays on the device).
 inline std::uint64_t count_node_iterator_n(const Graph& g,
                                            OrderKind order = OrderKind::by_degree()) {
   detail::use_order(g, order);
@@ -185,8 +340,15 @@ inline std::uint64_t count_node_iterator_n(const Graph& g,
   return t;
 }
 
-/// sequential.hpp:48-70 NodeIterator++ under `order` (the reference passes
-/// the OrderRank itself).
+/// sequential.hpp:48-70 NodeIterator++ (the reference's signature takes the
+/// OrderRank; an OrderKind works too).
+inline std::uint64_t count_node_iterator_pp(const Graph& g, const OrderRank& order,
+                                            bool use_intersection = false) {
+  detail::use_order(g, order);
+  std::uint64_t t = 0;
+  detail::check(tg_count_node_iterator_pp(g.handle(), use_intersection ? 1 : 0, &t));
+  return t;
+}
 inline std::uint64_t count_node_iterator_pp(const Graph& g, OrderKind order = OrderKind::by_degree(),
                                             bool use_intersection = false) {
   detail::use_order(g, order);
@@ -196,6 +358,12 @@ inline std::uint64_t count_node_iterator_pp(const Graph& g, OrderKind order = Or
 }
 
 /// sequential.hpp:95-104 under `order` (default ByDegree).
+inline std::uint64_t ordering_cost(const Graph& g, const OrderRank& order) {
+  detail::use_order(g, order);
+  std::uint64_t c = 0;
+  detail::check(tg_ordering_cost(g.handle(), &c));
+  return c;
+}
 inline std::uint64_t ordering_cost(const Graph& g, OrderKind order = OrderKind::by_degree()) {
   detail::use_order(g, order);
   std::uint64_t c = 0;
@@ -385,6 +553,12 @@ inline std::map<std::pair<NodeId, NodeId>, std::uint64_t> per_edge_triangle_coun
       if (u < adj[i]) out[{u, adj[i]}] = te[k++];
   return out;
 }
+/// sequential.hpp:108-122 with the reference's signature: t_e does not
+/// depend on the order the EffectiveAdjacency was built under.
+inline std::map<std::pair<NodeId, NodeId>, std::uint64_t> per_edge_triangle_counts(
+    const Graph& g, const EffectiveAdjacency&) {
+  return per_edge_triangle_counts(g);
+}
 
 /// sparsify.hpp:113-155 variance_report.
 struct VarianceReport {
@@ -429,7 +603,7 @@ inline Graph build_graph_from_text(std::string_view text, std::size_t n_override
   std::uint64_t line = 0;
   const tg_status st = tg_graph_from_text(device, text.data(), text.size(), n_override, &h, &line);
   detail::check(st, line);
-  return Graph(h);
+  return Graph(h, device);
 }
 
 /// io.hpp:52-64 write_edge_list, on the device.

@@ -62,6 +62,10 @@ SIGNATURES = {
     "tg_graph_csr": (_i32, [_vp, _vp, _vp]),
     "tg_set_stream": (_i32, [_vp, _vp]),
     "tg_set_order": (_i32, [_vp, _i32, _u64]),
+    "tg_set_order_rank": (_i32, [_vp, _vp]),
+    "tg_eff_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pvp]),
+    "tg_eff_free": (_i32, [_vp]),
+    "tg_eff_count": (_i32, [_vp, _pu64, _vp, _vp, _u64, _i32, _pu64]),
     "tg_graph_from_text": (_i32, [C.c_int, _vp, _u64, _u64, _pvp, _pu64]),
     "tg_parse_edge_list": (_i32, [C.c_int, _vp, _u64, _vp, _u64, _pu64, _pu64]),
     "tg_write_edge_list": (_i32, [_vp, _vp, _u64, _pu64]),

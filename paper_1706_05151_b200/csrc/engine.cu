@@ -150,6 +150,7 @@ tg_graph* new_graph(int device) {
 // oriented CSR and rank partitions are dropped when the order changes.
 void apply_order(tg_graph* g, int kind, uint64_t seed) {
   TG_REQUIRE(kind >= TG_ORDER_BY_ID && kind <= TG_ORDER_BY_CORENESS, "unknown order kind");
+  // (a caller's OrderRank, TG_ORDER_RANK, is only set by tg_set_order_rank)
   const uint64_t sd = kind == TG_ORDER_BY_RANDOM ? seed : 0;
   if (g->g.order == kind && g->g.order_seed == sd) return;
   tgb::set_order(g->g, kind, sd, g->stream);
@@ -889,6 +890,29 @@ tg_status tg_set_order(tg_graph* g, int32_t kind, uint64_t seed) {
   });
 }
 
+tg_status tg_set_order_rank(tg_graph* g, const uint32_t* rank) {
+  return guard([&] {
+    enter(g);
+    const uint64_t n = g->g.n;
+    TG_REQUIRE(rank != nullptr || n == 0, "null rank");
+    if (n && !is_device_ptr(rank)) {  // OrderRank::rank is a permutation (order.hpp:31-33)
+      std::vector<uint8_t> seen(n, 0);
+      for (uint64_t v = 0; v < n; ++v) {
+        TG_REQUIRE(rank[v] < n && !seen[rank[v]], "OrderRank: rank must be a permutation of [0, n)");
+        seen[rank[v]] = 1;
+      }
+    }
+    upload(g->g.okey, rank, n, g->stream);
+    g->g.order = TG_ORDER_RANK;
+    g->g.order_seed = 0;
+    g->have_eff = false;
+    g->have_part = false;
+    g->have_rk = false;
+    g->rank_mode = -1;
+    sync(g);  // the caller's rank buffer may die on return
+  });
+}
+
 tg_status tg_coreness(tg_graph* g, uint64_t* core) {
   return guard([&] {
     enter(g);
@@ -1290,6 +1314,153 @@ tg_status tg_surrogate_count_device(tg_graph* g, const uint32_t* boundaries, uin
     });
     sync(g);  // moff is freed on return
   });
+}
+
+// ---- EffectiveAdjacency as a value (effective.hpp:17-35) ------------------
+
+struct tg_eff {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t n = 0;
+  tgb::DevEff e;
+  tgb::IntersectScratch scr;
+};
+
+tg_status tg_eff_from_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* entries,
+                          tg_eff** out) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr && offsets != nullptr, "null argument");
+    TG_REQUIRE(n <= 0xFFFFFFFFull, "n must fit NodeId");
+    int count = 0;
+    TG_CUDA(cudaGetDeviceCount(&count));
+    TG_REQUIRE(device >= 0 && device < count, "invalid CUDA device ordinal");
+    TG_CUDA(cudaSetDevice(device));
+    uint64_t m = 0;
+    const bool dev = is_device_ptr(offsets);
+    if (dev) {
+      TG_CUDA(cudaMemcpy(&m, offsets + n, 8, cudaMemcpyDeviceToHost));
+    } else {
+      m = offsets[n];
+      TG_REQUIRE(offsets[0] == 0, "EffectiveAdjacency: offsets[0] must be 0");
+      for (uint64_t v = 0; v < n; ++v) TG_REQUIRE(offsets[v] <= offsets[v + 1], "offsets must be sorted");
+      TG_REQUIRE(entries != nullptr || m == 0, "null entries");
+      if (m && !is_device_ptr(entries))
+        for (uint64_t v = 0; v < n; ++v)
+          for (uint64_t k = offsets[v]; k < offsets[v + 1]; ++k)
+            TG_REQUIRE(entries[k] < n && (k == offsets[v] || entries[k - 1] < entries[k]),
+                       "EffectiveAdjacency: lists must be ID-sorted, ids < n");
+    }
+    auto* h = new tg_eff;
+    try {
+      h->device = device;
+      TG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->n = n;
+      DevEff& e = h->e;
+      e.rows = n;
+      e.entries = m;
+      e.base = 0;
+      e.compact = true;
+      upload(e.off, offsets, n + 1, h->stream);
+      e.data.alloc(m + tgb::kQuadPad, h->stream);
+      TG_CUDA(cudaMemsetAsync(e.data.p, 0, (m + tgb::kQuadPad) * 4, h->stream));
+      if (m)
+        TG_CUDA(cudaMemcpyAsync(e.data.p, entries, m * 4,
+                                is_device_ptr(entries) ? cudaMemcpyDeviceToDevice
+                                                       : cudaMemcpyHostToDevice, h->stream));
+      tgb::eff_desc_from_off(e, h->stream);
+      TG_CUDA(cudaStreamSynchronize(h->stream));
+    } catch (...) {
+      tg_eff_free(h);
+      throw;
+    }
+    *out = h;
+  });
+}
+
+tg_status tg_eff_free(tg_eff* h) {
+  if (!h) return TG_OK;
+  return guard([&] {
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    h->e.off.release();
+    h->e.desc.release();
+    h->e.data.release();
+    h->scr.big.release();
+    h->scr.big_count.release();
+    if (h->stream) {
+      cudaStreamSynchronize(h->stream);
+      cudaStreamDestroy(h->stream);
+    }
+    delete h;
+  });
+}
+
+tg_status tg_eff_count(tg_eff* h, uint64_t* total, uint64_t* tally, uint32_t* triples,
+                       uint64_t capacity, int32_t raw, uint64_t* num_triangles) {
+  tg_status cap_status = TG_OK;
+  tg_status st = guard([&] {
+    TG_REQUIRE(h != nullptr, "null EffectiveAdjacency handle");
+    TG_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const uint64_t n = h->n;
+    const uint32_t N = (uint32_t)n;
+    const CsrView v = view(h->e);
+    DBuf<unsigned long long> ctr(1, s), tv, cursor;
+    ctr.zero();
+    unsigned long long T = 0;
+    if (n)  // the count (and the listing's exact size)
+      tgb::intersect_rows(v, 0, N, v, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, h->scr, s,
+                          h->e.data.n, true);
+    download(&T, ctr.p, 1, s);
+    TG_CUDA(cudaStreamSynchronize(s));
+    if (total) *total = T;
+    if (num_triangles) *num_triangles = T;
+    if (!tally && !triples) return;
+    DBuf<uint32_t> tri;
+    uint32_t* list_out = nullptr;
+    bool direct = false;
+    if (triples) {
+      direct = is_device_ptr(triples) && capacity >= T;
+      if (direct) {
+        list_out = triples;
+      } else {
+        tri.alloc(3 * (T ? T : 1), s);
+        list_out = tri.p;
+      }
+      cursor.alloc(1, s);
+      cursor.zero();
+    }
+    unsigned long long* tp = nullptr;
+    if (tally) {
+      if (is_device_ptr(tally)) {
+        tp = (unsigned long long*)tally;
+        TG_CUDA(cudaMemsetAsync(tp, 0, n * 8, s));
+      } else {
+        tv.alloc(n ? n : 1, s);
+        tv.zero();
+        tp = tv.p;
+      }
+    }
+    ctr.zero();
+    CountOut out{ctr.p, tp, list_out, triples ? cursor.p : nullptr, triples ? T : 0};
+    out.raw = raw != 0;
+    if (n) tgb::intersect_rows(v, 0, N, v, 0, N, out, h->scr, s, h->e.data.n, true);
+    if (tally && tv.p) download(tally, (const uint64_t*)tv.p, n, s);
+    if (triples && !direct) {
+      const uint64_t words = 3 * std::min<uint64_t>(T, capacity);
+      if (words)
+        TG_CUDA(cudaMemcpyAsync(triples, tri.p, words * 4,
+                                is_device_ptr(triples) ? cudaMemcpyDeviceToDevice
+                                                       : cudaMemcpyDeviceToHost, s));
+    }
+    if (triples && capacity < T) cap_status = TG_ERR_CAPACITY;
+    TG_CUDA(cudaStreamSynchronize(s));
+  });
+  if (st == TG_OK && cap_status != TG_OK) {
+    t_last_error = "triangle capacity smaller than the triangle count";
+    return cap_status;
+  }
+  return st;
 }
 
 }  // extern "C"

@@ -88,11 +88,14 @@ __device__ __forceinline__ bool contains_u32(const uint32_t* a, uint32_t n, uint
 
 __device__ __forceinline__ void emit_triple(const CountOut& out, unsigned long long pos, uint32_t a,
                                             uint32_t b, uint32_t c) {
-  // ListSink normalisation (sequential.hpp:39-44)
-  uint32_t t;
-  if (a > b) { t = a; a = b; b = t; }
-  if (b > c) { t = b; b = c; c = t; }
-  if (a > b) { t = a; a = b; b = t; }
+  // ListSink normalisation (sequential.hpp:39-44), unless the raw sink
+  // order (v, u, w) is asked for
+  if (!out.raw) {
+    uint32_t t;
+    if (a > b) { t = a; a = b; b = t; }
+    if (b > c) { t = b; b = c; c = t; }
+    if (a > b) { t = a; a = b; b = t; }
+  }
   if (pos < out.cap) {
     out.tri[3 * pos + 0] = a;
     out.tri[3 * pos + 1] = b;

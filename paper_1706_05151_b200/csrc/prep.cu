@@ -1073,6 +1073,14 @@ void orient_full_gappy(const DevGraph& g, DevEff& out, cudaStream_t s) {
   else launch_orient_gappy<32>(g, out.desc.p, out.data.p, s);
 }
 
+void eff_desc_from_off(DevEff& e, cudaStream_t s) {
+  e.desc.alloc(e.rows ? e.rows : 1, s);
+  if (!e.rows) return;
+  k_desc_from_off<<<grid_for(e.rows, 256), 256, 0, s>>>(e.off.p, e.rows, e.desc.p);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s) {
   const uint64_t rows = in.rows;
   out.rows = rows;

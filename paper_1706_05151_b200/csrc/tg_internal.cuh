@@ -184,6 +184,8 @@ void ready_chunks(const DevEff& e, const uint32_t* d_cb, uint32_t K, uint32_t k,
                   uint32_t ve, uint8_t* ready, cudaStream_t s);
 void select_ready(const uint8_t* ready, uint32_t vb, uint32_t ve, uint32_t k, uint32_t* ids,
                   unsigned long long* cnt, cudaStream_t s);
+// desc of a compact oriented CSR from its offsets (e.off, e.rows set).
+void eff_desc_from_off(DevEff& e, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
 // sum of the lengths of the lists longer than thr (host result).
@@ -234,6 +236,9 @@ struct CountOut {
   uint32_t* tri;               // device 3*cap or nullptr (ListSink)
   unsigned long long* cursor;  // device, listing cursor
   uint64_t cap;
+  // listing: raw (apex v, middle u, w) as emitted by count_node_iterator_n's
+  // sink call (sequential.hpp:82-86) instead of the ListSink normalisation
+  bool raw = false;
 };
 
 // Rank-labelled view for the bitmap CTA path (ctab.cuh): rank[v] = position

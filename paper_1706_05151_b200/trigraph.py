@@ -5,7 +5,8 @@ Names, argument meaning and error behaviour follow
 libtrigraph_b200.so on the GPU.  Deviations, all documented in DESIGN.md:
 
 * ``Graph`` is device-resident (one CUDA device per Graph).
-* The order is always ByDegree (the north_star path; order.hpp:95-104).
+* Every OrderKind is supported (ByDegree, the north_star path, is the
+  default; order.hpp:85-128), and so is a caller-supplied ``OrderRank``.
 * ``ExecMode`` is accepted for signature parity and ignored: device results
   are mode-independent (acceptance.cpp:438-468).
 * ``RankStats.realized_cost`` is algorithmic work (sum of h_v + h_u over the
@@ -226,6 +227,12 @@ def _order(kind, seed: int = 0) -> OrderKind:
 
 
 def _use_order(g: "Graph", kind) -> None:
+    if isinstance(kind, OrderRank):  # order.hpp:31-35, a caller's permutation
+        r = np.ascontiguousarray(kind.rank, dtype=np.uint32)
+        if r.shape[0] != g.num_nodes():
+            raise ValueError("OrderRank: rank must have num_nodes() entries")
+        check(lib().tg_set_order_rank(g._h, _p(r) if r.size else None))
+        return
     o = _order(kind)
     check(lib().tg_set_order(g._h, int(o.tag), int(o.seed)))
 
@@ -307,10 +314,16 @@ def compute_order(g: Graph, kind=None) -> OrderRank:
     return OrderRank(r[:n])
 
 
-@dataclass
 class EffectiveAdjacency:  # effective.hpp:17-35
-    offsets: np.ndarray
-    entries: np.ndarray
+    """N_v lists (ID-sorted) as host arrays, EffectiveAdjacency(offsets, eff)
+    (effective.hpp:18-20).  Counting it (count_node_iterator_n) adopts a copy
+    on ``device`` once (tg_eff_from_csr) and runs there."""
+
+    def __init__(self, offsets, entries, device: int = 0):
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        self.entries = np.ascontiguousarray(entries, dtype=np.uint32)
+        self.device = device
+        self._h = None
 
     def num_nodes(self) -> int:
         return self.offsets.shape[0] - 1
@@ -324,21 +337,105 @@ class EffectiveAdjacency:  # effective.hpp:17-35
     def effdeg(self, v: int) -> int:
         return int(self.offsets[v + 1] - self.offsets[v])
 
+    def _handle(self):
+        if self._h is None:
+            h = C.c_void_p()
+            check(lib().tg_eff_from_csr(self.device, self.num_nodes(), _p(self.offsets),
+                                        _p(self.entries) if self.entries.size else None,
+                                        C.byref(h)))
+            self._h = h
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().tg_eff_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
 
 def effective_adjacency(g: Graph, order=None) -> EffectiveAdjacency:
-    """effective.hpp:37-52 under ``order`` (default by_degree), oriented on
-    the device."""
+    """effective.hpp:37-52 under ``order`` -- an OrderKind / name (default
+    by_degree) or an OrderRank from compute_order (the reference's
+    effective_adjacency(g, order)) -- oriented on the device."""
     _use_order(g, order)
     n, m = g._info()
     off = np.zeros(n + 1, dtype=np.uint64)
     eff = np.zeros(max(m, 1), dtype=np.uint32)
     check(lib().tg_effective_adjacency(g._h, _p(off), _p(eff)))
-    return EffectiveAdjacency(off, eff[:m])
+    return EffectiveAdjacency(off, eff[:m], g.device)
 
 
-def count_node_iterator_n(g: Graph, order=None) -> int:
-    """sequential.hpp:74-91 count over effective_adjacency(g, order)
-    (default by_degree)."""
+class NullSink:  # sequential.hpp:19-21
+    def __call__(self, v, u, w):
+        pass
+
+
+class NodeTallySink:  # sequential.hpp:24-33
+    def __init__(self, n: int):
+        self.counts = np.zeros(n, dtype=np.uint64)
+
+    def __call__(self, v, u, w):
+        self.counts[v] += 1
+        self.counts[u] += 1
+        self.counts[w] += 1
+
+
+class ListSink:  # sequential.hpp:36-46
+    def __init__(self):
+        self.triangles = np.zeros((0, 3), dtype=np.uint32)
+
+    def __call__(self, v, u, w):
+        t = np.sort(np.array([[v, u, w]], dtype=np.uint32), axis=1)
+        self.triangles = np.concatenate([self.triangles, t])
+
+
+def _eff_count(e: EffectiveAdjacency, sink):
+    h = e._handle()
+    n = e.num_nodes()
+    t, nt = C.c_uint64(), C.c_uint64()
+    if sink is None or isinstance(sink, NullSink):
+        check(lib().tg_eff_count(h, C.byref(t), None, None, 0, 0, C.byref(nt)))
+        return t.value
+    if isinstance(sink, NodeTallySink):  # device TALLY path
+        tv = np.zeros(max(n, 1), dtype=np.uint64)
+        check(lib().tg_eff_count(h, C.byref(t), _p(tv), None, 0, 0, C.byref(nt)))
+        sink.counts[:n] += tv[:n]
+        return t.value
+    check(lib().tg_eff_count(h, C.byref(t), None, None, 0, 0, C.byref(nt)))
+    T = t.value
+    tri = np.zeros((max(T, 1), 3), dtype=np.uint32)
+    raw = 0 if isinstance(sink, ListSink) else 1
+    check(lib().tg_eff_count(h, C.byref(t), None, _p(tri), T, raw, C.byref(nt)))
+    tri = tri[:T]
+    if isinstance(sink, ListSink):  # device LIST path (normalised triples)
+        sink.triangles = np.concatenate([sink.triangles, tri])
+        return T
+    # any callable sink(v, u, w): raw device listing, replayed on the host in
+    # the reference's emission order -- v ascending, u along the ID-sorted
+    # N_v, w ascending (sequential.hpp:78-86)
+    tri = tri[np.lexsort((tri[:, 2], tri[:, 1], tri[:, 0]))]
+    for v, u, w in tri.tolist():
+        sink(v, u, w)
+    return T
+
+
+def count_node_iterator_n(g, sink=None, order=None) -> int:
+    """sequential.hpp:74-91.  ``g``: an EffectiveAdjacency (the reference's
+    count_node_iterator_n(eff, sink)) -- ``sink`` None / NullSink (count),
+    NodeTallySink / ListSink (the device sinks) or any callable (v, u, w),
+    called once per triangle in the reference's order -- or a Graph
+    (counted over effective_adjacency(g, order), default by_degree)."""
+    if isinstance(g, EffectiveAdjacency):
+        return _eff_count(g, sink)
+    if isinstance(sink, (OrderKind, OrderTag, OrderRank, str, int)):
+        sink, order = None, sink  # count_node_iterator_n(g, order)
+    if sink is not None and not isinstance(sink, NullSink):
+        return _eff_count(effective_adjacency(g, order), sink)
     _use_order(g, order)
     t = C.c_uint64()
     check(lib().tg_count(g._h, C.byref(t)))

@@ -43,7 +43,7 @@ def test_library_is_sm100a():
 
 def test_cpp_mirror_compiles_and_links(tmp_path):
     exe = tmp_path / "parity_main"
-    cmd = ["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
            os.path.join(ROOT, "tests", "cpp", "parity_main.cpp"), "-o", str(exe),
            _lib.LIB_PATH, f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,5 +1,6 @@
 """Run the reference's own test cases through the C++ mirror on the B200
-(tests/cpp/parity_main.cpp, namespace alias trigraph = trigraph_b200)."""
+(tests/cpp/parity_main.cpp: test_sequential.cpp / test_engines.cpp cases
+copied unchanged under the namespace alias trigraph = trigraph_b200)."""
 import os
 import subprocess
 
@@ -13,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_cpp_mirror_runs_reference_cases(tmp_path):
     exe = tmp_path / "parity_main"
-    cmd = ["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
            os.path.join(ROOT, "tests", "cpp", "parity_main.cpp"), "-o", str(exe), _lib.LIB_PATH,
            f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
