@@ -259,21 +259,23 @@ class CpuBaseline:
                                           C.byref(tb), C.byref(e), C.byref(t), C.byref(st))
         return float(dt), tb.value, e.value, t.value, st.value
 
-    def seq(self, r: int):
-        """One 1-thread sample: (seconds, edges, triangles)."""
-        s = self.ranges(r % self.R)
+    def seq(self, r: int, core: int):
+        """One 1-thread sample, sub-range r of one core: (seconds, edges,
+        triangles)."""
+        s = self.ranges(r % self.R)[2 * core: 2 * core + 2].copy()
         e, t = C.c_uint64(), C.c_uint64()
-        dt = self.O.ref().ref_seq_sample(self.h, C.c_void_p(s.ctypes.data), self.threads,
+        dt = self.O.ref().ref_seq_sample(self.h, C.c_void_p(s.ctypes.data), 1,
                                          C.byref(e), C.byref(t))
         return float(dt), e.value, t.value
 
     def calibrate(self, target_s: float):
-        """Pick R (sub-ranges per core) so one all-core sample counts for
-        ~target_s seconds."""
-        dt, _, _, _, _ = self.aop(0)
-        full = dt * self.R
-        self.R = max(1, min(1 << 16, int(round(full / max(target_s, 1e-3)))))
-        log(f"[cpu] calibration: full all-core count ~{full:.0f}s -> R={self.R}")
+        """Pick R (sub-ranges per core) so one all-core sample -- partition
+        building plus counting -- takes ~target_s seconds."""
+        self.R = 1024
+        dt, tb, _, _, _ = self.aop(0)
+        full = (dt + tb) * self.R
+        self.R = max(1, min(1 << 20, int(round(full / max(target_s, 1e-3)))))
+        log(f"[cpu] calibration: full all-core build+count ~{full:.0f}s -> R={self.R}")
 
     def report(self, samples: int = 3, seq_budget_s: float = 8.0):
         rates = [self.aop(17 * k + 1) for k in range(samples)]
@@ -283,8 +285,8 @@ class CpuBaseline:
         st = sum(x[4] for x in rates)
         s_t = s_e = 0
         k = 0
-        while s_t < seq_budget_s and k < 64:
-            dt, e, _ = self.seq(31 * k + 5)
+        while s_t < seq_budget_s and k < 4 * self.threads:
+            dt, e, _ = self.seq(31 * k + 5, k % self.threads)
             s_t += dt
             s_e += e
             k += 1
@@ -298,8 +300,9 @@ class CpuBaseline:
                 "partition_stored_entries": st,
                 "one_thread": {"value": s_e / s_t if s_t > 0 else None, "unit": UNIT,
                                "cores": 1,
-                               "sample": f"count_node_iterator_n loop over {k} x {self.threads} "
-                                         f"sub-ranges ({s_e} oriented edges, {s_t:.2f}s)"},
+                               "sample": f"count_node_iterator_n loop over {k} sub-ranges "
+                                         f"(1/{self.R} of a core each; {s_e} oriented edges, "
+                                         f"{s_t:.2f}s)"},
                 "setup_s": self.setup_s}
 
 
@@ -580,11 +583,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=3)
     ap.add_argument("--cpu-step-s", type=float, default=3.0,
-                    help="all-core counting seconds per CPU-baseline sample")
-    ap.add_argument("--cpu-seq-s", type=float, default=8.0)
-    ap.add_argument("--ref-step-s", type=float, default=1.5,
-                    help="--impl reference: all-core counting seconds per step")
-    ap.add_argument("--ref-seq-s", type=float, default=8.0)
+                    help="all-core build + count seconds per CPU-baseline sample")
+    ap.add_argument("--cpu-seq-s", type=float, default=6.0)
+    ap.add_argument("--ref-step-s", type=float, default=2.0,
+                    help="--impl reference: all-core build + count seconds per step")
+    ap.add_argument("--ref-seq-s", type=float, default=6.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

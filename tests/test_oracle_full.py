@@ -148,7 +148,7 @@ def test_bench_cpu_baseline_c1():
         cb.R = 7
         tot = sum(cb.aop(r)[3] for r in range(7))
         assert tot == 1269
-        s, e1, t1 = cb.seq(3)
+        s, e1, t1 = cb.seq(3, 1)
         assert s >= 0 and e1 > 0
     finally:
         cb.close()

@@ -7,7 +7,7 @@ name=$1; src=$2; shift 2
 R=$(cd "$(dirname "$0")/.." && pwd)
 C=$R/paper_1706_05151_b200/csrc
 make -s -C "$C"
-D=$R/variants/$name
+D=$R/exp_variants/$name
 mkdir -p "$D"
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
   -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr "$@" -c "$C/$src.cu" \
