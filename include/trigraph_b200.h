@@ -335,6 +335,10 @@ void tg_debug_set_rank_bitmap(int32_t mode, uint32_t cap_bits);
  * vertices); force_wide: 64-bit element indices in the scalar
  * intersection kernels (taken above 2^32 list slots).  All exact. */
 void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide);
+/* Test hook: the id-window encoding of the count (window.cu): 0 = automatic
+ * (when <= 10% of the oriented entries lie outside their row's 64-id
+ * window), 1 = always, 2 = never.  All exact. */
+void tg_debug_set_window(int32_t mode);
 /* Device-side time (ms) of the last intersection pass (CUDA events on the
  * launching stream); 0 if none. */
 double tg_last_intersect_ms(tg_graph* g);

@@ -37,6 +37,12 @@ struct tg_graph {
   bool have_rk = false;
   uint64_t rdata_gen = ~0ull;    // rdata matches eff iff rdata_gen == eff_gen
   tgb::DBuf<uint32_t> rk, rdata;
+  // window encoding (window.cu): -1 undecided, 0 off, 1 on (per order)
+  int window_mode = -1;
+  uint64_t window_far = 0;
+  uint64_t window_gen = ~0ull;   // win matches eff iff window_gen == eff_gen
+  tgb::WindowEff win;
+  tgb::DBuf<uint32_t> wdefer;
   tgb::IntersectScratch scr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
@@ -53,6 +59,7 @@ struct tg_graph {
   void for_each_buf(F&& f) {
     f(g.off); f(g.adj); f(g.deg); f(g.dcode); f(g.okey);
     f(eff.off); f(eff.data); f(eff.desc); f(rk); f(rdata);
+    f(win.rec); f(win.far); f(win.ctr); f(wdefer);
     f(scr.big); f(scr.big_count);
     f(part.off); f(part.data); f(part.desc);
     f(pack.desc); f(pack.doff);
@@ -158,6 +165,7 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
   g->have_part = false;
   g->have_rk = false;
   g->rank_mode = -1;
+  g->window_mode = -1;
 }
 
 // (Re)orient the whole graph (effective.hpp:37-52).
@@ -199,6 +207,36 @@ RankView rank_view(tg_graph* g) {
     g->rdata_gen = g->eff_gen;
   }
   return RankView{g->rk.p, g->rdata.p, (uint32_t)n, g_rank_cap ? g_rank_cap : (1u << 19)};
+}
+
+// The window encoding (window.cu) when it pays: automatic when at most 10%
+// of the oriented entries lie outside their row's 64-id window (decided once
+// per order from one counting pass), or as forced by tg_debug_set_window.
+// Rebuilt after every orientation.
+bool window_ready(tg_graph* g) {
+  if (tgb::g_window_mode == 2 || !g->g.n) return false;
+  cudaStream_t s = g->stream;
+  if (g->window_mode < 0) {
+    g->window_far = tgb::window_far_entries(g->eff, s);
+    g->window_mode = g->window_far * 10 <= g->eff.entries ? 1 : 0;
+  }
+  if (g->window_mode == 0 && tgb::g_window_mode != 1) return false;
+  if (g->window_gen != g->eff_gen) {
+    tgb::window_build(g->eff, g->window_far, g->win, s);
+    g->window_gen = g->eff_gen;
+  }
+  return true;
+}
+
+// NodeIteratorN over apexes [vlo, vhi) through the window encoding; the
+// deferred apexes (long far lists) through the generic kernels.
+void window_rows(tg_graph* g, uint32_t vlo, uint32_t vhi, unsigned long long* d_total) {
+  cudaStream_t s = g->stream;
+  tgb::window_count(g->win, vlo, vhi, d_total, g->wdefer, s);
+  const CsrView full = view(g->eff);
+  tgb::intersect_list(full, g->wdefer.p, g->win.ctr.p + 1, vhi - vlo, full,
+                      CountOut{d_total, nullptr, nullptr, nullptr, 0}, g->scr, s, g->eff.data.n,
+                      rank_view(g));
 }
 
 // Counting pass with CUDA-event timing of the intersection kernels.
@@ -419,9 +457,13 @@ uint64_t seq_count(tg_graph* g) {
   ctr.zero();
   const CsrView full = full_view(g);
   const uint32_t N = (uint32_t)g->g.n;
+  const bool win = window_ready(g);
   timed_pass(g, [&] {
-    tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                        g->eff.data.n, true, rank_view(g));
+    if (win)
+      window_rows(g, 0, N, ctr.p);
+    else
+      tgb::intersect_rows(full, 0, N, full, 0, N, CountOut{ctr.p, nullptr, nullptr, nullptr, 0},
+                          g->scr, s, g->eff.data.n, true, rank_view(g));
   });
   unsigned long long h = 0;
   download(&h, ctr.p, 1, s);
@@ -570,6 +612,8 @@ void tg_debug_set_rank_bitmap(int32_t mode, uint32_t cap_bits) {
   g_rank_bitmap = mode;
   g_rank_cap = cap_bits ? std::max<uint32_t>(32, (cap_bits + 31) & ~31u) : 0;
 }
+
+void tg_debug_set_window(int32_t mode) { tgb::g_window_mode = mode; }
 
 void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide) {
   tgb::g_orient_mode = orient_mode;
@@ -909,6 +953,7 @@ tg_status tg_set_order_rank(tg_graph* g, const uint32_t* rank) {
     g->have_part = false;
     g->have_rk = false;
     g->rank_mode = -1;
+    g->window_mode = -1;
     sync(g);  // the caller's rank buffer may die on return
   });
 }
@@ -1179,10 +1224,14 @@ tg_status tg_step_device(tg_graph* g, uint64_t* d_total) {
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
     const CsrView full = full_view(g);
     const uint32_t N = (uint32_t)g->g.n;
+    const bool win = window_ready(g);
     timed_pass(g, [&] {
-      tgb::intersect_rows(full, 0, N, full, 0, N,
-                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                          g->eff.data.n, true, rank_view(g));
+      if (win)
+        window_rows(g, 0, N, (unsigned long long*)d_total);
+      else
+        tgb::intersect_rows(full, 0, N, full, 0, N,
+                            CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0},
+                            g->scr, s, g->eff.data.n, true, rank_view(g));
     });
   });
 }
@@ -1203,10 +1252,14 @@ tg_status tg_count_device(tg_graph* g, uint64_t* d_total) {
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
     const CsrView full = full_view(g);
     const uint32_t N = (uint32_t)g->g.n;
+    const bool win = window_ready(g);
     timed_pass(g, [&] {
-      tgb::intersect_rows(full, 0, N, full, 0, N,
-                          CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
-                          g->eff.data.n, true, rank_view(g));
+      if (win)
+        window_rows(g, 0, N, (unsigned long long*)d_total);
+      else
+        tgb::intersect_rows(full, 0, N, full, 0, N,
+                            CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0},
+                            g->scr, s, g->eff.data.n, true, rank_view(g));
     });
   });
 }
@@ -1231,8 +1284,11 @@ tg_status tg_aop_rank_device(tg_graph* g, const uint32_t* boundaries, uint64_t p
     const CsrView full = full_view(g);
     const uint32_t N = (uint32_t)g->g.n;
     const uint32_t cb = boundaries[rank], ce = boundaries[rank + 1];
+    const bool win = ce > cb && window_ready(g);
     timed_pass(g, [&] {
-      if (ce > cb)
+      if (win)
+        window_rows(g, cb, ce, (unsigned long long*)d_total);
+      else if (ce > cb)
         tgb::intersect_rows(full, cb, ce, full, 0, N,
                             CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0}, g->scr, s,
                           g->eff.data.n, true, rank_view(g));

@@ -289,6 +289,26 @@ void intersect_msgs(const MsgView& msgs, CsrView nu, uint32_t ulo, uint32_t uhi,
 void clustering_device(const DevGraph& g, const unsigned long long* d_tally, double* d_c,
                        cudaStream_t s);
 
+// ---- window.cu: local-id-window encoding of the oriented lists ----
+// mask bit i <-> v-32+i ∈ N_v; F_v = the rest (inline in the row's 32-byte
+// record up to 5 entries, else in far[]).  For graphs whose entries are
+// mostly within 32 ids of their row (Watts-Strogatz).
+struct WindowEff {
+  DBuf<uint4> rec;  // 2 per row: {mask, |F_v|, F_v inline (<= 5) or its position in far}
+  DBuf<uint32_t> far;
+  DBuf<unsigned long long> ctr;  // [0] far cursor, [1] deferred apexes
+  uint64_t rows = 0;
+};
+// entries of e outside their row's window (host result, one sync)
+uint64_t window_far_entries(const DevEff& e, cudaStream_t s);
+// (re)build w from e; far_cap >= window_far_entries(e)
+void window_build(const DevEff& e, uint64_t far_cap, WindowEff& w, cudaStream_t s);
+// NodeIteratorN over apexes [vlo, vhi) into *d_total; apexes with long far
+// lists are written to defer (count at w.ctr.p + 1) for the generic kernels
+void window_count(WindowEff& w, uint32_t vlo, uint32_t vhi, unsigned long long* d_total,
+                  DBuf<uint32_t>& defer, cudaStream_t s);
+extern int g_window_mode;  // 0 auto, 1 force on, 2 off (tests)
+
 // ---- analytics.cu (sequential.hpp:48-70, 108-122, sparsify.hpp:113-155) ----
 // count_node_iterator_pp under g's current order (host result).
 uint64_t node_iterator_pp_device(const DevGraph& g, cudaStream_t s);

@@ -13,7 +13,7 @@ mkdir -p "$D"
   -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr "$@" -c "$C/$src.cu" \
   -o "$D/$src.o" 2> "$D/ptxas.log"
 objs=""
-for o in prep intersect exchange engine sparsify analytics order io gen; do
+for o in prep intersect exchange engine sparsify analytics order io gen window; do
   if [ "$o" = "$src" ]; then objs="$objs $D/$o.o"; else objs="$objs $C/build/$o.o"; fi
 done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared \

@@ -49,6 +49,14 @@ def main():
     ap.add_argument("--engines", action="store_true")
     a = ap.parse_args()
     L = lib()
+    if os.environ.get("TG_L2_FETCH"):  # experiment: cudaLimitMaxL2FetchGranularity (bytes)
+        torch.cuda.init()
+        rt = C.CDLL("libcudart.so.12")
+        v = C.c_size_t(int(os.environ["TG_L2_FETCH"]))
+        assert rt.cudaDeviceSetLimit(5, v) == 0
+        got = C.c_size_t()
+        rt.cudaDeviceGetLimit(C.byref(got), 5)
+        print("L2 fetch granularity", got.value, file=sys.stderr)
     if os.environ.get("TG_WARP_VARIANT"):
         L.tg_debug_set_warp_variant(int(os.environ["TG_WARP_VARIANT"]))
     if os.environ.get("TG_RANK_BITMAP") or os.environ.get("TG_RANK_CAP"):
