@@ -49,6 +49,19 @@ def main():
     ap.add_argument("--engines", action="store_true")
     a = ap.parse_args()
     L = lib()
+    if os.environ.get("TG_L2_PERSIST"):  # experiment: cudaLimitPersistingL2CacheSize (bytes)
+        torch.cuda.init()
+        rt = C.CDLL("libcudart.so.12")
+        mx = C.c_int()
+        rt.cudaDeviceGetAttribute(C.byref(mx), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+        win = C.c_int()
+        rt.cudaDeviceGetAttribute(C.byref(win), 109, 0)  # cudaDevAttrMaxAccessPolicyWindowSize
+        want = min(int(os.environ["TG_L2_PERSIST"]), mx.value)
+        assert rt.cudaDeviceSetLimit(6, C.c_size_t(want)) == 0
+        got = C.c_size_t()
+        rt.cudaDeviceGetLimit(C.byref(got), 6)
+        print("persisting L2 max", mx.value, "window max", win.value, "set", got.value,
+              file=sys.stderr)
     if os.environ.get("TG_L2_FETCH"):  # experiment: cudaLimitMaxL2FetchGranularity (bytes)
         torch.cuda.init()
         rt = C.CDLL("libcudart.so.12")
