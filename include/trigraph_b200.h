@@ -306,6 +306,59 @@ tg_status tg_surrogate_count_device(tg_graph* g, const uint32_t* boundaries, uin
                                     uint64_t rank, const uint32_t* d_hdr, uint64_t num_msgs,
                                     const uint32_t* d_data, uint64_t* d_total);
 
+/* ---- across GPUs: one rank per GPU (comm.cu) ----
+ *
+ * The engines with their real exchange (engines.hpp:38-76, 146-198,
+ * 211-268).  Every rank holds rows [lo, hi) of the symmetric CSR (the ranks'
+ * ranges tile [0, n) in rank order) and the global degrees -- a graph from
+ * tg_graph_from_rows -- or the whole graph (then its rows are an equal-
+ * adjacency-volume split).  Each rank orients only its rows.  One C++ host
+ * can drive N devices: create the communicators, then call each rank's
+ * entry points from its own host thread.  NCCL is loaded at run time. */
+typedef struct tg_comm tg_comm;
+/* ncclGetUniqueId: 128 bytes for tg_comm_init, made on one rank and
+ * shared with the others by the caller. */
+tg_status tg_comm_unique_id(void* id128);
+/* ncclCommInitRank on `device`. */
+tg_status tg_comm_init(int device, int nranks, int rank, const void* id128, tg_comm** out);
+/* nranks in-process ranks (one host thread each) on devices[r]: the
+ * exchange is host-orchestrated device copies (tests; no NCCL needed). */
+tg_status tg_comm_init_local(int nranks, const int* devices, tg_comm** comms);
+tg_status tg_comm_free(tg_comm* c);
+tg_status tg_comm_info(tg_comm* c, int32_t* nranks, int32_t* rank);
+/* A rank-local Graph: rows [row_lo, row_hi) of the symmetric CSR of an
+ * n-vertex graph (offsets: row_hi - row_lo + 1 entries, any base; adj: the
+ * rows' entries) and every vertex's degree (n, host).  Counted only through
+ * the tg_*_comm entry points (it cannot orient the rows it does not hold). */
+tg_status tg_graph_from_rows(int device, uint64_t n, uint32_t row_lo, uint32_t row_hi,
+                             const uint64_t* offsets, const uint32_t* adj,
+                             const uint32_t* degrees, tg_graph** out);
+/* run_engine (engines.hpp:335-418) across the communicator, Aop or
+ * AnopSurrogate, counts (no sinks, no sparsification, degree order):
+ *  Aop       -- own rows oriented, the oriented rows gathered (one broadcast
+ *               per rank), the cfg->cost plan from the gathered costs, the
+ *               rank's core counted, one all-reduce of T;
+ *  Surrogate -- own rows oriented, list lengths gathered, the plan from
+ *               distributed costs, oriented rows moved to their core owner
+ *               (one all-to-allv: Σ stored = m), the (v, N_v) messages
+ *               exchanged (all-to-allv), SurrogateCount.
+ * Every rank returns the same total, per_rank (nranks) and boundaries
+ * (nranks+1); cfg->ranks must be 0 or nranks; cfg->boundaries overrides
+ * the plan. */
+tg_status tg_run_engine_comm(tg_graph* g, tg_comm* c, const tg_config* cfg, uint64_t* total,
+                             tg_rank_stats* per_rank, uint32_t* boundaries_out);
+/* One AOP step (the bench's N-GPU step): own rows oriented + gathered, the
+ * rank's core of `boundaries` (nranks+1) counted, T all-reduced into
+ * *d_total (device u64) on every rank. */
+tg_status tg_aop_step_comm(tg_graph* g, tg_comm* c, const uint32_t* boundaries, uint64_t* d_total);
+/* clustering_coefficients (engines.hpp:422-435) across the communicator:
+ * AOP tallies of the rank's apexes at all three corners, each core range
+ * summed at its owner (aggregate_clustering, engines.hpp:229-254), C_v
+ * there.  tally_core / cc_core: this rank's core [b_r, b_r+1) (host or
+ * device); boundaries_out: nranks+1. */
+tg_status tg_clustering_comm(tg_graph* g, tg_comm* c, const tg_config* cfg,
+                             uint32_t* boundaries_out, uint64_t* tally_core, double* cc_core);
+
 /* ---- diagnostics ---- */
 const char* tg_last_error(void);
 const char* tg_status_string(tg_status s);

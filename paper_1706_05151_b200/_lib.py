@@ -63,6 +63,15 @@ SIGNATURES = {
     "tg_set_stream": (_i32, [_vp, _vp]),
     "tg_set_order": (_i32, [_vp, _i32, _u64]),
     "tg_set_order_rank": (_i32, [_vp, _vp]),
+    "tg_comm_unique_id": (_i32, [_vp]),
+    "tg_comm_init": (_i32, [C.c_int, C.c_int, C.c_int, _vp, _pvp]),
+    "tg_comm_init_local": (_i32, [C.c_int, _vp, _vp]),
+    "tg_comm_free": (_i32, [_vp]),
+    "tg_comm_info": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "tg_graph_from_rows": (_i32, [C.c_int, _u64, _u32, _u32, _vp, _vp, _vp, _pvp]),
+    "tg_run_engine_comm": (_i32, [_vp, _vp, C.POINTER(TgConfig), _pu64, _vp, _vp]),
+    "tg_aop_step_comm": (_i32, [_vp, _vp, _vp, _vp]),
+    "tg_clustering_comm": (_i32, [_vp, _vp, C.POINTER(TgConfig), _vp, _vp, _vp]),
     "tg_eff_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pvp]),
     "tg_eff_free": (_i32, [_vp]),
     "tg_eff_count": (_i32, [_vp, _pu64, _vp, _vp, _u64, _i32, _pu64]),

@@ -22,49 +22,9 @@
 #include <mutex>
 
 #include "exchange.cuh"
+#include "handle.cuh"
 #include "tg_internal.cuh"
 
-struct tg_graph {
-  int device = 0;
-  cudaStream_t own = nullptr;
-  cudaStream_t stream = nullptr;
-  tgb::DevGraph g;
-  bool have_eff = false;
-  tgb::DevEff eff;
-  uint64_t eff_gen = 0;          // bumped by every (re)orientation
-  // bitmap CTA path (ctab.cuh): order rank + rank-labelled lists
-  int rank_mode = -1;            // -1 undecided, 0 off, 1 on (per order)
-  bool have_rk = false;
-  uint64_t rdata_gen = ~0ull;    // rdata matches eff iff rdata_gen == eff_gen
-  tgb::DBuf<uint32_t> rk, rdata;
-  // window encoding (window.cu): -1 undecided, 0 off, 1 on (per order)
-  int window_mode = -1;
-  uint64_t window_far = 0;
-  uint64_t window_gen = ~0ull;   // win matches eff iff window_gen == eff_gen
-  tgb::WindowEff win;
-  tgb::DBuf<uint32_t> wdefer;
-  tgb::IntersectScratch scr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  bool timed = false;
-  // rank-local caches (multi-process surrogate)
-  bool have_part = false;
-  uint64_t part_rank = 0;
-  std::vector<uint32_t> part_b;
-  tgb::DevEff part;
-  tgb::SurrogatePack pack;
-
-  // every device buffer the handle owns (release before the stream dies;
-  // re-home stream-ordered frees when the caller switches streams)
-  template <class F>
-  void for_each_buf(F&& f) {
-    f(g.off); f(g.adj); f(g.deg); f(g.dcode); f(g.okey);
-    f(eff.off); f(eff.data); f(eff.desc); f(rk); f(rdata);
-    f(win.rec); f(win.far); f(win.ctr); f(wdefer);
-    f(scr.big); f(scr.big_count);
-    f(part.off); f(part.data); f(part.desc);
-    f(pack.desc); f(pack.doff);
-  }
-};
 
 namespace {
 
@@ -170,6 +130,8 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
 
 // (Re)orient the whole graph (effective.hpp:37-52).
 void orient(tg_graph* g) {
+  TG_REQUIRE(!g->partial,
+             "a rank-local graph (tg_graph_from_rows) is oriented by the tg_*_comm entry points");
   tgb::orient_full(g->g, g->eff, g->stream);
   g->have_eff = true;
   ++g->eff_gen;
@@ -582,6 +544,30 @@ tg_status graph_from_generator(int device, uint64_t n_override, tg_graph** out, 
   });
 }
 }  // namespace
+
+namespace tgh {  // the helpers above, for comm.cu
+tg_graph* new_graph(int device) { return ::new_graph(device); }
+void enter(tg_graph* g) { ::enter(g); }
+void sync(tg_graph* g) { ::sync(g); }
+void ensure_eff(tg_graph* g) { ::ensure_eff(g); }
+tgb::CsrView view(const tgb::DevEff& e) { return ::view(e); }
+tgb::CsrView full_view(tg_graph* g) { return ::full_view(g); }
+tgb::RankView rank_view(tg_graph* g) { return ::rank_view(g); }
+bool window_ready(tg_graph* g) { return ::window_ready(g); }
+void window_rows(tg_graph* g, uint32_t vlo, uint32_t vhi, unsigned long long* d_total) {
+  ::window_rows(g, vlo, vhi, d_total);
+}
+std::vector<uint32_t> plan_for(tg_graph* g, int cost, uint64_t p, const uint32_t* override_b) {
+  return ::plan_for(g, cost, p, override_b);
+}
+bool is_device_ptr(const void* p) { return ::is_device_ptr(p); }
+void install_eff(tg_graph* g, tgb::DevEff&& e) {
+  g->eff = std::move(e);
+  g->have_eff = true;
+  ++g->eff_gen;
+  g->have_part = false;
+}
+}  // namespace tgh
 
 extern "C" {
 

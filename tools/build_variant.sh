@@ -13,9 +13,9 @@ mkdir -p "$D"
   -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr "$@" -c "$C/$src.cu" \
   -o "$D/$src.o" 2> "$D/ptxas.log"
 objs=""
-for o in prep intersect exchange engine sparsify analytics order io gen window; do
+for o in prep intersect exchange engine sparsify analytics order io gen window comm; do
   if [ "$o" = "$src" ]; then objs="$objs $D/$o.o"; else objs="$objs $C/build/$o.o"; fi
 done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared \
-  -o "$D/libtrigraph_b200.so" $objs "$C/build/generators.o" -lpthread
+  -o "$D/libtrigraph_b200.so" $objs "$C/build/generators.o" -lpthread -ldl
 grep -A3 -E "k_intersect_warpILb0ELb0ELb0ELb0ENS0_8RowsApex|k_orient_tilesILi2ELb0E" "$D/ptxas.log" | grep -E "registers|spill" || true
