@@ -12,9 +12,12 @@ A step = one pass of the hot path over the graph resident in HBM:
 degree-ordered orientation (effective_adjacency, effective.hpp:37-52) +
 NodeIteratorN intersection over every oriented edge (sequential.hpp:74-91).
 value = oriented edges (m) processed per second by the whole job.
-At N GPUs (torchrun), rank i runs the AOP rank body for core i of the
-DPD cost-balanced plan (partition.hpp:116-141, engines.hpp:38-54) and the
-count is summed with one NCCL all-reduce; total work is fixed (strong scaling).
+At N GPUs (torchrun), the step is csrc/comm.cu's AOP step: rank i orients
+its 1/N of the rows, the oriented rows are broadcast in rank order over
+NVLink (NCCL) while rank i counts the apexes of core i of the DPD
+cost-balanced plan (partition.hpp:116-141, engines.hpp:38-54) whose lists
+arrived, and T is summed with one all-reduce; total work is fixed (strong
+scaling).
 
 e2e = the same metric through the reference-facing C ABI with HOST buffers:
 tg_count_from_csr (pinned host CSR -> HBM in vertex chunks, each chunk
@@ -397,17 +400,21 @@ def run_ours(args):
     d_total = torch.zeros(1, dtype=torch.int64, device="cuda")
     dptr = C.c_void_p(d_total.data_ptr())
 
-    if ws > 1:
-        plan = T.compute_boundaries(g, T.CostKind.Dpd, ws).boundaries
-        bptr = C.c_void_p(plan.ctypes.data)
+    use_comm = ws > 1 or args.force_comm
+    if use_comm:
+        # one NCCL communicator over the job (csrc/comm.cu): each rank orients
+        # its 1/N of the rows, the oriented rows are broadcast in rank order
+        # over NVLink while each rank counts the apexes of its DPD core whose
+        # lists arrived; one all-reduce of T
+        from paper_1706_05151_b200 import comm as M
+
+        comm = (M.Comm.from_process_group(local) if ws > 1
+                else M.Comm.init(local, 1, 0, M.Comm.unique_id()))
+        plan = M.run_engine_comm(g, comm, T.EngineConfig(engine=T.EngineKind.Aop)).boundaries
 
         def step():
-            check(L.tg_orient_device(g._h))
-            ev_mid.append(torch.cuda.Event(enable_timing=True))
-            ev_mid[-1].record(stream)
-            d_total.zero_()
-            check(L.tg_aop_rank_device(g._h, bptr, ws, rank, dptr))
-            dist.all_reduce(d_total)
+            M.aop_step_comm(g, comm, plan, d_total.data_ptr())
+            ev_mid.append(None)
     else:
         def step():
             check(L.tg_orient_device(g._h))
@@ -443,7 +450,9 @@ def run_ours(args):
     launches = L.tg_kernel_launches() - launches0
     clk = clocks.stop()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    isect_ms = [mid.elapsed_time(e) for mid, e in zip(ev_mid, ends)]
+    # (the N-GPU step overlaps its count with the transfers: no separate
+    # intersection time -- the step is the figure)
+    isect_ms = step_ms if use_comm else [mid.elapsed_time(e) for mid, e in zip(ev_mid, ends)]
     tot_ms = starts[0].elapsed_time(ends[-1])
     if dist:
         t = torch.tensor([tot_ms], device="cuda")
@@ -461,21 +470,35 @@ def run_ours(args):
         isect_max = float(t.item())
 
     # ---- e2e through the public API with host buffers (N = 1: the streamed
-    # tg_count_from_csr; N > 1: distributed.count_aop_from_host_csr)
+    # tg_count_from_csr; N > 1: each rank uploads its rows + the degrees,
+    # tg_graph_from_rows, then the AOP step across the ranks)
     off_h, adj_h = g.csr()
-    off_p = torch.from_numpy(off_h.view(np.int64)).pin_memory()
-    adj_p = torch.from_numpy(adj_h.view(np.int32)).pin_memory()
+    if use_comm:
+        rows = M.split_rows(off_h, ws)
+        lo, hi = int(rows[rank]), int(rows[rank + 1])
+        deg_p = torch.from_numpy(np.diff(off_h).astype(np.uint32).view(np.int32)).pin_memory()
+        off_p = torch.from_numpy(off_h[lo:hi + 1].view(np.int64)).pin_memory()
+        adj_p = torch.from_numpy(adj_h[off_h[lo]:off_h[hi]].view(np.int32)).pin_memory()
+        h2d = off_p.numel() * 8 + adj_p.numel() * 4 + deg_p.numel() * 4
+    else:
+        off_p = torch.from_numpy(off_h.view(np.int64)).pin_memory()
+        adj_p = torch.from_numpy(adj_h.view(np.int32)).pin_memory()
+        h2d = off_p.numel() * 8 + adj_p.numel() * 4
     del off_h, adj_h
-    h2d = off_p.numel() * 8 + adj_p.numel() * 4
     e2e_t = []
     for i in range(args.e2e_warmup + args.e2e_steps):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        if dist:
-            from paper_1706_05151_b200.distributed import count_aop_from_host_csr
-            cnt = count_aop_from_host_csr(n, off_p, adj_p, plan, torch.device("cuda", local))
+        if use_comm:
+            gr = M.graph_from_rows(n, lo, hi, off_p.numpy().view(np.uint64),
+                                   adj_p.numpy().view(np.uint32), deg_p.numpy().view(np.uint32),
+                                   device=local)
+            check(L.tg_set_stream(gr._h, C.c_void_p(stream.cuda_stream)))
+            M.aop_step_comm(gr, comm, plan, d_total.data_ptr())
+            cnt = int(d_total.item())
+            gr.close()
         else:
             # one reference-facing call: Graph(n, offsets, adj) + by_degree
             # orientation + count, the upload streamed under the compute
@@ -512,7 +535,7 @@ def run_ours(args):
     # ---- roofline of the intersection pass: 4 bytes x W algorithmic elements
     peak, peak_kind = measured_peak()
     w_rank = W / ws if ws > 1 else W  # DPD balances W across ranks
-    achieved = 4.0 * w_rank / (isect_avg / 1e3) / 1e9
+    achieved = 4.0 * w_rank / (isect_avg / 1e3) / 1e9  # (N > 1: over the whole step)
     traffic, traffic_src = profile_traffic(args.config)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
@@ -540,14 +563,14 @@ def run_ours(args):
         "data": "synthetic (seeded generator of the config, bit-identical to the reference "
                 "gen_pa stream / the oracle's generators)",
         "config": {"workload": CONFIGS[args.config][2], "n": n, "m": m, "triangles": T_total,
-                   "parallelism": f"aop{ws}" if ws > 1 else "single",
+                   "parallelism": f"aop{ws}" if use_comm else "single",
                    "step": "orientation + intersection over the HBM-resident graph",
                    "l2": "inputs (CSR + oriented CSR) > 126 MB L2; no flush"},
         "intersections_per_s": value,
         # oriented edges / intersection time (kernel only, the
         # orientation excluded), slowest rank at N > 1
-        "kernel_only": {"edges_per_s": m / (isect_max / 1e3), "intersect_ms": isect_max,
-                        "orient_ms": orient_avg},
+        "kernel_only": ({"edges_per_s": m / (isect_max / 1e3), "intersect_ms": isect_max,
+                         "orient_ms": orient_avg} if not use_comm else None),
         "elements_per_s": W / (ms_per_step / 1e3),
         "build_graph": {"ms": build_ms, "pairs": E_pairs,
                         "path": "device pairs -> CSR (CUB radix sort + unique), CUDA events"},
@@ -559,10 +582,11 @@ def run_ours(args):
                 "h2d_only_ms": 1e3 * h2d_floor,  # bare copy of the same bytes (not the metric)
                 "path": ("tg_count_from_csr(pinned host CSR): chunked H2D overlapped with "
                          "orientation and the count of every apex whose lists arrived"
-                         if ws == 1 else
-                         "per rank: 1/N of the pinned host CSR uploaded, NCCL all-gather of "
-                         "the rest over NVLink, tg_count_from_csr_range (its DPD core), "
-                         "NCCL all-reduce of the 8-byte counts; max over ranks")},
+                         if not use_comm else
+                         "per rank: its rows of the pinned host CSR + the degrees uploaded "
+                         "(tg_graph_from_rows), tg_aop_step_comm (rows oriented, oriented rows "
+                         "broadcast over NVLink, core counted as lists arrive, all-reduce of "
+                         "T); max over ranks")},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -581,6 +605,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="the N-GPU step (csrc/comm.cu) even at N = 1 (tests)")
     ap.add_argument("--cpu-samples", type=int, default=3)
     ap.add_argument("--cpu-step-s", type=float, default=3.0,
                     help="all-core build + count seconds per CPU-baseline sample")

@@ -347,6 +347,10 @@ tg_status tg_graph_from_rows(int device, uint64_t n, uint32_t row_lo, uint32_t r
  * the plan. */
 tg_status tg_run_engine_comm(tg_graph* g, tg_comm* c, const tg_config* cfg, uint64_t* total,
                              tg_rank_stats* per_rank, uint32_t* boundaries_out);
+/* effective_adjacency for rows [row_lo, row_hi) alone (one rank's share of
+ * the orientation; *entries = its oriented entries).  Used by the per-rank
+ * projections (tools/scaling_projection.py). */
+tg_status tg_orient_rows_device(tg_graph* g, uint32_t row_lo, uint32_t row_hi, uint64_t* entries);
 /* One AOP step (the bench's N-GPU step): own rows oriented + gathered, the
  * rank's core of `boundaries` (nranks+1) counted, T all-reduced into
  * *d_total (device u64) on every rank. */
@@ -374,8 +378,7 @@ void tg_debug_set_chunk_entries(uint64_t entries);
  * oriented list is <= 16 entries, else one apex per warp iteration; 16-byte
  * quad loads when list indices fit 32 bits), 1 = scalar one-apex-per-warp and
  * scalar CTA path, 2 = quad apex groups, 3 = quad one-apex-per-warp, 4 =
- * scalar apex groups, 5 = lane-per-edge groups (lane.cuh), 6 = scalar groups
- * with id-window membership masks (groupn.cuh).  All exact. */
+ * scalar apex groups.  All exact. */
 void tg_debug_set_warp_variant(int32_t variant);
 /* Test hook: the bitmap CTA path (apexes whose rank window, n - rank(v) - 1,
  * fits cap_bits of shared memory; ctab.cuh).  mode 0 = automatic (on when

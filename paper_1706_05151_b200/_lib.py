@@ -71,6 +71,7 @@ SIGNATURES = {
     "tg_graph_from_rows": (_i32, [C.c_int, _u64, _u32, _u32, _vp, _vp, _vp, _pvp]),
     "tg_run_engine_comm": (_i32, [_vp, _vp, C.POINTER(TgConfig), _pu64, _vp, _vp]),
     "tg_aop_step_comm": (_i32, [_vp, _vp, _vp, _vp]),
+    "tg_orient_rows_device": (_i32, [_vp, _u32, _u32, _pu64]),
     "tg_clustering_comm": (_i32, [_vp, _vp, C.POINTER(TgConfig), _vp, _vp, _vp]),
     "tg_eff_from_csr": (_i32, [C.c_int, _u64, _vp, _vp, _pvp]),
     "tg_eff_free": (_i32, [_vp]),

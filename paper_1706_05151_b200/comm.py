@@ -107,13 +107,14 @@ def graph_from_rows(n: int, row_lo: int, row_hi: int, offsets, adj, degrees,
 
 
 def split_rows(off: np.ndarray, parts: int) -> np.ndarray:
-    """parts+1 row boundaries splitting a CSR into equal adjacency volume
-    (the default input distribution)."""
+    """parts+1 row boundaries splitting a CSR into equal adjacency volume,
+    rounded to whole 32-vertex tiles (the default input distribution; tile-
+    aligned rows orient with the one-pass tile kernel)."""
     n = off.shape[0] - 1
     tgt = (np.arange(parts + 1, dtype=np.float64) * float(off[-1]) / parts)
-    b = np.searchsorted(off, tgt, side="left").astype(np.uint32)
+    b = np.searchsorted(off, tgt, side="left").astype(np.uint64) & ~np.uint64(31)
     b[0], b[-1] = 0, n
-    return np.maximum.accumulate(b)
+    return np.maximum.accumulate(np.minimum(b, n)).astype(np.uint32)
 
 
 def run_engine_comm(g: Graph, comm: Comm, cfg: Optional[EngineConfig] = None) -> RunReport:
@@ -151,7 +152,7 @@ def clustering_comm(g: Graph, comm: Comm, cost: CostKind = CostKind.Dpd, boundar
                                 boundaries=boundaries))
     r = comm.rank
     b = np.zeros(p + 1, dtype=np.uint32)
-    # the core range is known after the plan: query it first with a null output
+    # (outputs sized n: the core range is known only once the plan is made)
     n = g.num_nodes()
     tv = np.zeros(max(n, 1), dtype=np.uint64)
     cc = np.zeros(max(n, 1), dtype=np.float64)

@@ -230,7 +230,8 @@ struct LocalTransport : Transport {
 
 __global__ void k_volume_split(const uint64_t* __restrict__ off, uint64_t n, uint32_t parts,
                                uint32_t* __restrict__ a) {
-  // a[j] = smallest v with off[v] >= j * off[n] / parts (a[0] = 0, a[parts] = n)
+  // a[j] = smallest v with off[v] >= j * off[n] / parts (a[0] = 0, a[parts] = n),
+  // rounded down to whole 32-vertex tiles (the tile kernel's unit)
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j > parts) return;
   if (j == 0) { a[0] = 0; return; }
@@ -242,7 +243,7 @@ __global__ void k_volume_split(const uint64_t* __restrict__ off, uint64_t n, uin
     if ((unsigned __int128)off[mid] * parts >= target) hi = mid;
     else lo = mid + 1;
   }
-  a[j] = (uint32_t)lo;
+  a[j] = (uint32_t)(lo & ~31ull);
 }
 
 __global__ void k_lens_from_off(const uint64_t* __restrict__ off, uint64_t rows,
@@ -423,7 +424,10 @@ void orient_mine(tg_graph* g, Transport& T, Oriented& o) {
   const uint64_t n = g->g.n;
   o.a = row_split(g, T);
   const uint32_t lo = o.a[T.rank], hi = o.a[T.rank + 1];
-  tgb::orient_rows(g->g, lo, hi, o.slice, s);
+  if (lo % 32 == 0 && (hi % 32 == 0 || hi == n))
+    tgb::orient_rows_tiles(g->g, lo, hi, o.slice, s);  // the one-pass tile kernel
+  else
+    tgb::orient_rows(g->g, lo, hi, o.slice, s);
   o.cnt = all_gather_host(T, {o.slice.entries}, s);
   o.lens.alloc(n ? n : 1, s);
   if (hi > lo) {
@@ -675,18 +679,104 @@ tg_status tg_graph_from_rows(int device, uint64_t n, uint32_t row_lo, uint32_t r
   });
 }
 
+tg_status tg_orient_rows_device(tg_graph* g, uint32_t row_lo, uint32_t row_hi, uint64_t* entries) {
+  return guard([&] {
+    tgh::enter(g);
+    TG_REQUIRE(row_lo <= row_hi && row_hi <= g->g.n, "invalid row range");
+    TG_REQUIRE(!g->partial || (row_lo >= g->row_lo && row_hi <= g->row_hi),
+               "rows outside the rank-local graph");
+    DevEff slice;
+    if (row_lo % 32 == 0 && (row_hi % 32 == 0 || row_hi == g->g.n))
+      tgb::orient_rows_tiles(g->g, row_lo, row_hi, slice, g->stream);
+    else
+      tgb::orient_rows(g->g, row_lo, row_hi, slice, g->stream);
+    if (entries) *entries = slice.entries;
+  });
+}
+
 tg_status tg_aop_step_comm(tg_graph* g, tg_comm* c, const uint32_t* boundaries, uint64_t* d_total) {
   return guard([&] {
     tgh::enter(g);
     TG_REQUIRE(c && boundaries && d_total, "null argument");
     Transport& T = *c->t;
-    const auto b = checked_boundaries(boundaries, T.size, g->g.n);
-    Oriented o;
-    aop_prepare(g, T, o);
+    const int N = T.size, r = T.rank;
+    const uint64_t n = g->g.n;
+    const auto b = checked_boundaries(boundaries, N, n);
     cudaStream_t s = g->stream;
+    // own rows oriented, every list length gathered: the compact layout of
+    // the full oriented CSR (offsets, descriptors) is fixed before any list
+    // arrives
+    Oriented o;
+    orient_mine(g, T, o);
+    uint64_t m = 0;
+    std::vector<uint64_t> base(N);
+    for (int k = 0; k < N; ++k) {
+      base[k] = m;
+      m += o.cnt[k];
+    }
+    DevEff full;
+    full.rows = n;
+    full.base = 0;
+    full.compact = true;
+    full.entries = m;
+    full.data.alloc(m + tgb::kQuadPad, s);
+    TG_CUDA(cudaMemsetAsync(full.data.p + m, 0, tgb::kQuadPad * 4, s));
+    if (o.slice.entries)
+      TG_CUDA(cudaMemcpyAsync(full.data.p + base[r], o.slice.data.p, o.slice.entries * 4,
+                              cudaMemcpyDeviceToDevice, s));
+    offsets_from_lens(o.lens, n, full.off, s);
+    full.desc.alloc(n ? n : 1, s);
+    if (n) {
+      tgb::k_desc_from_off2<<<tgb::grid_for(n, 256), 256, 0, s>>>(full.off.p, n, full.desc.p);
+      TG_CHECK_LAUNCH();
+      ++tgb::g_launches;
+    }
+    // the slices arrive in rank order (= id order) on a transfer stream; after
+    // slice k, every apex of this rank's core whose lists all arrived --
+    // ready chunk max(chunk(v), chunk(last of N_v)), lists being ID-sorted --
+    // is counted on the compute stream while slice k+1 is in flight
+    const uint32_t cb = b[r], ce = b[r + 1];
+    DBuf<uint32_t> d_a(N + 1, s), ids(ce > cb ? ce - cb : 1, s);
+    DBuf<uint8_t> ready(n ? n : 1, s);
+    DBuf<unsigned long long> cnt(1, s);
+    TG_CUDA(cudaMemcpyAsync(d_a.p, o.a.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
+    TG_CUDA(cudaMemsetAsync(ready.p, 0xff, n ? n : 1, s));
     TG_CUDA(cudaMemsetAsync(d_total, 0, 8, s));
-    count_core(g, b[T.rank], b[T.rank + 1], (unsigned long long*)d_total);
+    cudaStream_t xs;
+    cudaEvent_t ev_c, ev_x;
+    TG_CUDA(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+    TG_CUDA(cudaEventCreateWithFlags(&ev_c, cudaEventDisableTiming));
+    TG_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
+    TG_CUDA(cudaEventRecord(ev_c, s));  // own slice in place
+    TG_CUDA(cudaStreamWaitEvent(xs, ev_c, 0));
+    const CsrView fv = tgh::view(full);
+    try {
+      for (int k = 0; k < N; ++k) {
+        T.broadcast(full.data.p + base[k], o.cnt[k] * 4, k, xs);
+        TG_CUDA(cudaEventRecord(ev_x, xs));
+        TG_CUDA(cudaStreamWaitEvent(s, ev_x, 0));
+        const uint32_t vb = std::max(o.a[k], cb), ve = std::min(o.a[k + 1], ce);
+        tgb::ready_chunks(full, d_a.p, (uint32_t)N, (uint32_t)k, vb, ve, ready.p, s);
+        if (ce > cb) {
+          tgb::select_ready(ready.p, cb, ce, (uint32_t)k, ids.p, cnt.p, s);
+          tgb::intersect_list(fv, ids.p, cnt.p, ce - cb, fv,
+                              CountOut{(unsigned long long*)d_total, nullptr, nullptr, nullptr, 0},
+                              g->scr, s, full.data.n);
+        }
+      }
+    } catch (...) {
+      cudaStreamSynchronize(xs);
+      cudaStreamDestroy(xs);
+      cudaEventDestroy(ev_c);
+      cudaEventDestroy(ev_x);
+      throw;
+    }
+    TG_CUDA(cudaStreamSynchronize(xs));
+    TG_CUDA(cudaStreamDestroy(xs));
+    TG_CUDA(cudaEventDestroy(ev_c));
+    TG_CUDA(cudaEventDestroy(ev_x));
     T.all_reduce_u64(d_total, 1, s);
+    tgh::install_eff(g, std::move(full));
   });
 }
 

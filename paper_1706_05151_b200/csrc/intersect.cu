@@ -405,8 +405,6 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "quad.cuh"
 #include "ctaq.cuh"
 #include "groupq.cuh"
-#include "lane.cuh"
-#include "groupn.cuh"
 #include "ctab.cuh"
 
 template <bool TALLY, bool LIST, bool FILTER, bool WIDE, class Apex>
@@ -421,28 +419,6 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // tail; measured: scalar groups win on Watts-Strogatz (mean list 10), quad
   // groups on R-MAT (15.5), quad per-apex on PA (20).
   const int wv = g_warp_variant;
-  if (wv == 6) {  // groupn.cuh (measured slower than group.cuh on C4)
-    const unsigned ggrid = grid_for(items, kGWarps * 32, 148u * 5u);
-    uint64_t chunk = items / ((uint64_t)ggrid * kGWarps * 8);
-    chunk = chunk < 32 ? 32 : (chunk > 256 ? 256 : chunk);
-    k_intersect_groupn<TALLY, LIST, FILTER, WIDE, Apex><<<ggrid, kGWarps * 32, 0, s>>>(
-        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
-        (uint32_t)chunk);
-    TG_CHECK_LAUNCH();
-    ++g_launches;
-    return;
-  }
-  if (wv == 5) {  // lane-per-edge groups (lane.cuh)
-    const unsigned ggrid = grid_for(items, kLWarps * 32, 148u * 6u);
-    uint64_t chunk = items / ((uint64_t)ggrid * kLWarps * 8);
-    chunk = chunk < 32 ? 32 : (chunk > 256 ? 256 : chunk);
-    k_intersect_lane<TALLY, LIST, FILTER, Apex><<<ggrid, kLWarps * 32, 0, s>>>(
-        A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
-        (uint32_t)chunk);
-    TG_CHECK_LAUNCH();
-    ++g_launches;
-    return;
-  }
   const bool groups = wv == 0 ? nu.avg_len <= 16.f : (wv == 2 || wv == 4);
   const bool quads = nu.quad_ok && (wv == 0 ? (!groups || nu.avg_len >= 14.f) : (wv == 2 || wv == 3));
   if (!groups && quads) {  // one apex per warp iteration, quad loads

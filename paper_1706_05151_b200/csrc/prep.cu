@@ -993,6 +993,87 @@ void orient_chunk(const DevGraph& g, DevEff& out, uint32_t vb, uint32_t ve, uint
   g_launches += 3;
 }
 
+// Rows [lo, hi) (lo a multiple of 32, hi too unless hi = n) with the
+// one-pass tile kernel -- one rank's share of the orientation: the tiles of
+// the range into a tile-layout scratch holding only the range's slots (the
+// kernels address it through base pointers shifted by -off[lo] / -lo), big
+// vertices above the range's slots, then one gather into the compact
+// layout of orient_rows (off / desc / data, base lo).
+void orient_rows_tiles(const DevGraph& g, uint32_t lo, uint32_t hi, DevEff& out, cudaStream_t s) {
+  TG_REQUIRE(lo % 32 == 0 && (hi % 32 == 0 || hi == g.n) && lo <= hi && hi <= g.n,
+             "orient_rows_tiles: rows must start on a 32-vertex tile");
+  const uint64_t rows = hi - lo;
+  uint64_t ob[2] = {0, 0};
+  TG_CUDA(cudaMemcpyAsync(&ob[0], g.off.p + lo, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaMemcpyAsync(&ob[1], g.off.p + hi, 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  const uint64_t span = ob[1] - ob[0];  // the range's symmetric slots
+  // scratch: the range's slots + its big vertices' lists (<= span) + padding
+  DevEff tile;
+  tile.desc.alloc(rows ? rows : 1, s);
+  tile.data.alloc(2 * span + kQuadPad, s);
+  // big-vertex queue: medium ones from the front, hubs from index hi-1 down
+  // (the kernels' convention with n = hi)
+  DBuf<uint32_t> bigq(hi ? hi : 1, s);
+  DBuf<unsigned long long> ctr(6, s);
+  ctr.zero();
+  uint64_t* desc_base = tile.desc.p - lo;
+  uint32_t* data_base = tile.data.p - ob[0];
+  if (rows) {
+    const uint64_t t_lo = lo / 32, t_hi = ((uint64_t)hi + 31) / 32;
+    const unsigned grid = grid_for(t_hi - t_lo, kOWarps, 148u * kOBlocks);
+    const bool coded = order_coded(g);
+    if (coded)
+      k_orient_tiles<2, true><<<grid, kOWarps * 32, 0, s>>>(
+          g.off.p, g.adj.p, order_key(g), g.dcode.p, hi, nullptr, desc_base, data_base, ctr.p,
+          bigq.p, ctr.p + 1, nullptr, nullptr, t_lo, t_hi);
+    else
+      k_orient_tiles<2, false><<<grid, kOWarps * 32, 0, s>>>(
+          g.off.p, g.adj.p, order_key(g), g.dcode.p, hi, nullptr, desc_base, data_base, ctr.p,
+          bigq.p, ctr.p + 1, nullptr, nullptr, t_lo, t_hi);
+    TG_CHECK_LAUNCH();
+    // big vertices' lists above the range's slots (relative position span)
+    if (coded)
+      k_orient_big1<true><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p,
+                                                  bigq.p, hi, ctr.p, ob[1], desc_base, data_base);
+    else
+      k_orient_big1<false><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p,
+                                                   bigq.p, hi, ctr.p, ob[1], desc_base, data_base);
+    TG_CHECK_LAUNCH();
+    g_launches += 2;
+  }
+  // compact copy, base lo
+  out.rows = rows;
+  out.base = lo;
+  out.compact = true;
+  out.off.alloc(rows + 1, s);
+  out.desc.alloc(rows ? rows : 1, s);
+  TG_CUDA(cudaMemsetAsync(out.off.p, 0, 8, s));
+  uint64_t entries = 0;
+  if (rows) {
+    DBuf<uint64_t> lens(rows, s);
+    k_desc_lens<<<grid_for(rows, 256), 256, 0, s>>>(tile.desc.p, rows, lens.p);
+    TG_CHECK_LAUNCH();
+    cub_run(s, [&](void* t, size_t& b) {
+      return cub::DeviceScan::InclusiveSum(t, b, lens.p, out.off.p + 1, (int64_t)rows, s);
+    });
+    TG_CUDA(cudaMemcpyAsync(&entries, out.off.p + rows, 8, cudaMemcpyDeviceToHost, s));
+    TG_CUDA(cudaStreamSynchronize(s));
+  }
+  out.entries = entries;
+  out.data.alloc(entries + kQuadPad, s);
+  TG_CUDA(cudaMemsetAsync(out.data.p + entries, 0, kQuadPad * 4, s));
+  if (rows) {
+    CsrView v{tile.desc.p, data_base, 0};
+    k_gather_compact<<<grid_for(rows * 32, 256, 148u * 32u), 256, 0, s>>>(v, rows, out.off.p,
+                                                                        out.data.p);
+    TG_CHECK_LAUNCH();
+    k_desc_from_off<<<grid_for(rows, 256), 256, 0, s>>>(out.off.p, rows, out.desc.p);
+    TG_CHECK_LAUNCH();
+    g_launches += 4;
+  }
+}
+
 void ready_chunks(const DevEff& e, const uint32_t* d_cb, uint32_t K, uint32_t k, uint32_t vb,
                   uint32_t ve, uint8_t* ready, cudaStream_t s) {
   if (ve <= vb) return;

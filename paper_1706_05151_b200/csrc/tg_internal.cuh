@@ -167,6 +167,9 @@ void compute_degrees(DevGraph& g, cudaStream_t s);
 // Orient rows [vlo, vhi) of g into `out` (out.base = vlo), compact layout;
 // lists ID-sorted.
 void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s);
+// The same output from the one-pass tile kernel (vlo a multiple of 32, vhi
+// too unless vhi = n): one rank's share of the full orientation.
+void orient_rows_tiles(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s);
 // Orient the whole graph (no host sync): one-pass tile layout, or compact.
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s);
 void orient_full_compact(const DevGraph& g, DevEff& out, cudaStream_t s);

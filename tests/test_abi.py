@@ -50,6 +50,16 @@ def test_cpp_mirror_compiles_and_links(tmp_path):
     assert r.returncode == 0, r.stderr
 
 
+def test_cpp_comm_driver_compiles_and_links(tmp_path):
+    exe = tmp_path / "comm_main"
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I",
+           "/usr/local/cuda/include", os.path.join(ROOT, "tests", "cpp", "comm_main.cpp"), "-o",
+           str(exe), _lib.LIB_PATH, f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lpthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
 def test_host_validation_maps_to_reference_exceptions():
     with pytest.raises(ValueError):
         T._cfg(T.EngineConfig(engine=T.EngineKind.Aop, ranks=2, boundaries=[0, 1]))

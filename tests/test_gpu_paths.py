@@ -28,7 +28,7 @@ GRAPHS = {
 
 @pytest.mark.parametrize("graph", sorted(GRAPHS))
 @pytest.mark.parametrize("orient_mode,force_wide,variant", [
-    (1, 0, 0), (5, 0, 0), (6, 0, 0), (1, 1, 1), (1, 1, 4), (6, 1, 1), (2, 1, 4), (1, 1, 5), (1, 0, 6), (2, 1, 6)])
+    (1, 0, 0), (5, 0, 0), (6, 0, 0), (1, 1, 1), (1, 1, 4), (6, 1, 1), (2, 1, 4)])
 def test_forced_large_graph_paths(graph, orient_mode, force_wide, variant):
     pairs = GRAPHS[graph]()
     ref = O.build_graph(pairs)
