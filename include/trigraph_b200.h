@@ -395,6 +395,12 @@ void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide);
  * (when <= 10% of the oriented entries lie outside their row's 64-id
  * window), 1 = always, 2 = never.  All exact. */
 void tg_debug_set_window(int32_t mode);
+/* Test hook: the slab layout of the oriented lists (each list's first 32
+ * entries in its own 128-byte-aligned slab, so the intersection reads a list
+ * as one DRAM line without a descriptor; slab.cuh): 0 = automatic (mean
+ * list > 16, <= 2% of the entries in lists longer than a slab), 1 = always,
+ * 2 = never.  All exact. */
+void tg_debug_set_slab(int32_t mode);
 /* Device-side time (ms) of the last intersection pass (CUDA events on the
  * launching stream); 0 if none. */
 double tg_last_intersect_ms(tg_graph* g);

@@ -110,6 +110,7 @@ SIGNATURES = {
     "tg_debug_set_warp_variant": (None, [_i32]),
     "tg_debug_set_paths": (None, [_i32, _i32]),
     "tg_debug_set_window": (None, [_i32]),
+    "tg_debug_set_slab": (None, [_i32]),
     "tg_debug_set_rank_bitmap": (None, [_i32, _u32]),
     "tg_gen_pa": (_i32, [_u64, _u64, _u64, _pvp, _pu64]),
     "tg_gen_gnp": (_i32, [_u64, _dbl, _u64, _pvp, _pu64]),

@@ -61,7 +61,9 @@ using tgb::DBuf;
 using tgb::DevEff;
 
 CsrView view(const DevEff& e) {
-  return CsrView{e.desc.p, e.data.p, e.base, e.rows ? (float)e.entries / (float)e.rows : 0.f};
+  CsrView v{e.desc.p, e.data.p, e.base, e.rows ? (float)e.entries / (float)e.rows : 0.f};
+  v.slab = e.slab;
+  return v;
 }
 
 bool is_device_ptr(const void* p) {
@@ -126,13 +128,41 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
   g->have_rk = false;
   g->rank_mode = -1;
   g->window_mode = -1;
+  g->slab_mode = -1;
+  g->g.slab = 0;
 }
 
-// (Re)orient the whole graph (effective.hpp:37-52).
+// (Re)orient the whole graph (effective.hpp:37-52).  The first orientation
+// under an order also decides the layout: the slab layout (one 128-byte line
+// per list, no descriptor on the intersection's random reads) when the
+// per-apex kernel would run (mean list > 16: PA-like graphs), at most 2% of
+// the entries sit in lists longer than a slab and none is longer than 4096;
+// or as forced by tg_debug_set_slab.
 void orient(tg_graph* g) {
   TG_REQUIRE(!g->partial,
              "a rank-local graph (tg_graph_from_rows) is oriented by the tg_*_comm entry points");
+  if (g->slab_mode >= 0 && g->slab_for != tgb::g_slab_mode) {
+    g->slab_mode = -1;
+    g->g.slab = 0;
+  }
   tgb::orient_full(g->g, g->eff, g->stream);
+  if (g->slab_mode < 0) {
+    g->slab_for = tgb::g_slab_mode;
+    g->slab_mode = 0;
+    const uint64_t n = g->g.n, m = g->g.m2 / 2;
+    if (tgb::g_slab_mode != 2 && n && n < 0xffffffffull && (tgb::g_orient_mode & 3) == 0) {
+      const tgb::SlabStats st = tgb::slab_stats(g->g, g->eff, g->stream);
+      const bool fits = n * tgb::kSlab + g->g.big_entries + st.extra_slots + tgb::kQuadPad < (1ull << 34);
+      const bool pays = m > 16 * n && st.long_entries * 50 <= m && st.max_len <= 4096;
+      if (fits && (pays || tgb::g_slab_mode == 1)) {
+        g->slab_mode = 1;
+        g->g.slab = tgb::kSlab;
+        g->g.slab_extra = st.extra_slots;
+        g->eff.data.release();  // (the tile-layout buffer; the slabs are sized anew)
+        tgb::orient_full(g->g, g->eff, g->stream);
+      }
+    }
+  }
   g->have_eff = true;
   ++g->eff_gen;
 }
@@ -600,6 +630,7 @@ void tg_debug_set_rank_bitmap(int32_t mode, uint32_t cap_bits) {
 }
 
 void tg_debug_set_window(int32_t mode) { tgb::g_window_mode = mode; }
+void tg_debug_set_slab(int32_t mode) { tgb::g_slab_mode = mode; }
 
 void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide) {
   tgb::g_orient_mode = orient_mode;

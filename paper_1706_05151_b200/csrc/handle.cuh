@@ -21,6 +21,9 @@ struct tg_graph {
   bool have_rk = false;
   uint64_t rdata_gen = ~0ull;    // rdata matches eff iff rdata_gen == eff_gen
   tgb::DBuf<uint32_t> rk, rdata;
+  // slab layout of the oriented lists: -1 undecided, 0 off, 1 on (per order;
+  // decided under slab_for = the g_slab_mode in force)
+  int slab_mode = -1, slab_for = 0;
   // window encoding (window.cu): -1 undecided, 0 off, 1 on (per order)
   int window_mode = -1;
   uint64_t window_far = 0;

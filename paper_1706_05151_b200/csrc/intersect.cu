@@ -35,6 +35,7 @@ struct RowsApex {
   CsrView view;
   uint32_t vlo, vhi;
   __device__ __forceinline__ uint64_t count() const { return vhi - vlo; }
+  __device__ __forceinline__ uint32_t vertex(uint64_t k) const { return vlo + (uint32_t)k; }
   __device__ __forceinline__ void get(uint64_t k, uint32_t& v, const uint32_t*& L,
                                       uint32_t& hv) const {
     v = vlo + (uint32_t)k;
@@ -50,6 +51,7 @@ struct ListApex {
   const uint32_t* ids;
   const unsigned long long* n;
   __device__ __forceinline__ uint64_t count() const { return *n; }
+  __device__ __forceinline__ uint32_t vertex(uint64_t k) const { return ids[k]; }
   __device__ __forceinline__ void get(uint64_t k, uint32_t& v, const uint32_t*& L,
                                       uint32_t& hv) const {
     v = ids[k];
@@ -403,6 +405,7 @@ k_intersect_warp(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #include "cta.cuh"
 #include "group.cuh"
 #include "quad.cuh"
+#include "slab.cuh"
 #include "ctaq.cuh"
 #include "groupq.cuh"
 #include "ctab.cuh"
@@ -419,6 +422,21 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
   // tail; measured: scalar groups win on Watts-Strogatz (mean list 10), quad
   // groups on R-MAT (15.5), quad per-apex on PA (20).
   const int wv = g_warp_variant;
+  // slab layout (apex lists = nu's own slabs): one DRAM line per N_u, no
+  // descriptors -- the per-apex slab kernel whatever the list lengths
+  if constexpr (!std::is_same<Apex, MsgApex>::value) {
+    if (nu.slab && A.view.data == nu.data && A.view.desc == nu.desc && (wv == 0 || wv == 3)) {
+      const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kSlabBlocks);  // resident
+      uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);
+      chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
+      k_intersect_slab<TALLY, LIST, FILTER, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
+          A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
+          (uint32_t)chunk);
+      TG_CHECK_LAUNCH();
+      ++g_launches;
+      return;
+    }
+  }
   const bool groups = wv == 0 ? nu.avg_len <= 16.f : (wv == 2 || wv == 4);
   const bool quads = nu.quad_ok && (wv == 0 ? (!groups || nu.avg_len >= 14.f) : (wv == 2 || wv == 3));
   if (!groups && quads) {  // one apex per warp iteration, quad loads

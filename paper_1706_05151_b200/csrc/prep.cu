@@ -28,6 +28,7 @@ namespace tgb {
 
 unsigned long long g_launches = 0;
 int g_orient_mode = 0;
+int g_slab_mode = 0;
 
 namespace {
 
@@ -247,7 +248,11 @@ constexpr uint32_t kOHub = 4096;  // ... and above which a whole CTA orients it 
 //          eff[tile_b + k] -- each tile's lists back to back at the start of
 //          the tile's own adjacency range (ID-sorted, vertex order), no mask,
 //          no scan; big vertices write above m2 (k_orient_big1).
-template <int MODE, bool CODED>
+//   SLAB : ONE mode writing the slab layout instead: list v
+//          in the 32-slot, 128-byte-aligned slab eff[32v, 32v+32), kNoEntry
+//          padded; vertices with h_v > 32 are re-oriented by k_orient_big1
+//          (full list above the slabs, its first 32 entries in the slab).
+template <int MODE, bool CODED, bool SLAB = false>
 __global__ void __launch_bounds__(kOWarps * 32, kOBlocks)
 k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode, uint64_t n,
@@ -260,7 +265,9 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
   __shared__ uint32_t sTbl[kOWarps][kOTbl + kOUnroll];
   __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
   __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
+  __shared__ uint32_t sHb[SLAB ? kOWarps : 1][32];  // kept entries of the tile before a segment
   constexpr bool FILL = MODE == 1, ONE = MODE == 2;
+  static_assert(!SLAB || ONE, "the slab layout is written by the one-pass mode");
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
@@ -279,6 +286,16 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     const uint64_t tile_b = __shfl_sync(FULL, my_b, 0);
     const uint32_t len = (uint32_t)(my_e - my_b);
     const bool big = len > kOBig;
+    if (SLAB) {  // pad the tile's 32 slabs (4 KB, 8 coalesced 16-byte stores per lane)
+      uint4* Q = reinterpret_cast<uint4*>(eff);
+      const uint64_t qend = n * (kSlab / 4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint64_t qi = v0 * (kSlab / 4) + 32 * j + lane;
+        if (qi < qend) Q[qi] = make_uint4(kNoEntry, kNoEntry, kNoEntry, kNoEntry);
+      }
+      __syncwarp();  // ordered before the entries written below
+    }
     if (!FILL && !ONE && big) bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
     if (ONE && big) {  // hubs (> kOHub) from the back of the queue, one CTA each
       if (len > kOHub) bigq[n - 1 - atomicAdd(bigq_n + 2, 1ull)] = (uint32_t)v;
@@ -295,7 +312,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     est -= elen;
     if (S == 0) {
       if (valid && !big) {
-        if (ONE) edesc[v] = make_desc(0, 0);
+        if (ONE) edesc[v] = make_desc(SLAB ? v * kSlab : 0, 0);
         else if (!FILL) cnt_or_eoff[v] = 0;
         else edesc[v] = make_desc(cnt_or_eoff[v], 0);
       }
@@ -395,7 +412,16 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
             const unsigned km = __ballot_sync(FULL, keep);
             const uint32_t send = __shfl_sync(FULL, c_end, jj);
             if (idx < wend && idx + 1 == send) sCum[w][jj] = kept + __popc(km & le_mask);
-            if (ONE && keep) eff[tile_b + kept + __popc(km & lt_mask)] = us[q];
+            if (SLAB) {
+              // rank of a kept entry in its own list = kept entries of the tile
+              // before it - those before its segment's first item
+              const uint32_t sst = __shfl_sync(FULL, c_st, jj);
+              const uint32_t before = kept + __popc(km & lt_mask);
+              if (idx < wend && idx == sst) sHb[w][jj] = before;
+              __syncwarp();
+              const uint32_t r = before - sHb[w][jj & 31u];  // (idle lanes: any slot)
+              if (keep && r < kSlab) eff[(uint64_t)sv * kSlab + r] = us[q];
+            } else if (ONE && keep) eff[tile_b + kept + __popc(km & lt_mask)] = us[q];
             if (!ONE && lane == 0 && km) {  // record the decisions for the FILL pass
               const uint64_t pos = tile_b + base;
               const uint32_t sh = (uint32_t)(pos & 31);
@@ -416,7 +442,11 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
         hb = c ? sCum[w][c - 1] : 0u;
         h = sCum[w][c] - hb;
       }
-      if (ONE) edesc[v] = make_desc(tile_b + hb, h);
+      if (SLAB) {
+        edesc[v] = make_desc(v * kSlab, h);
+        // longer than a slab: whole list above the slabs (k_orient_big1)
+        if (h > kSlab) bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
+      } else if (ONE) edesc[v] = make_desc(tile_b + hb, h);
       else cnt_or_eoff[v] = h;
     }
     __syncwarp();
@@ -499,7 +529,9 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
 // Counters: c[1] medium queue size, c[2] region cursor, c[3] hub queue size,
 // c[4] hub claims, c[5] medium claims.
 constexpr int kBigU = 4;
-template <bool CODED>
+// SLAB: the first kSlab kept entries also go to v's slab (padded by the tile
+// kernel), and the queue holds the non-big vertices with h_v > kSlab too.
+template <bool CODED, bool SLAB = false>
 __global__ void __launch_bounds__(256)
 k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
               const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode,
@@ -564,14 +596,17 @@ k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj
       __syncthreads();
       for (int ch = 0; ch < 32; ++ch) {
         const uint32_t km = sM[32 * w + ch];
-        if ((km >> lane) & 1u)
-          eff[ob + kept + sO[32 * w + ch] + __popc(km & lt_mask)] =
-              __ldg(adj + wb + 32 * ch + lane);
+        if ((km >> lane) & 1u) {
+          const uint64_t r = kept + sO[32 * w + ch] + __popc(km & lt_mask);
+          const uint32_t x = __ldg(adj + wb + 32 * ch + lane);
+          eff[ob + r] = x;
+          if (SLAB && r < kSlab) eff[(uint64_t)v * kSlab + r] = x;
+        }
       }
       kept += tot;
       __syncthreads();  // sM / sO / sW reused by the next segment
     }
-    if (t == 0) edesc[v] = make_desc(ob, kept);
+    if (t == 0) edesc[v] = (SLAB && kept <= kSlab) ? make_desc((uint64_t)v * kSlab, kept) : make_desc(ob, kept);
   }
   // medium big vertices: one warp each, claimed dynamically
   const uint64_t nq = c[1];
@@ -602,11 +637,16 @@ k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj
         const bool keep =
             k0 + 32 * q + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg);
         const unsigned km = __ballot_sync(FULL, keep);
-        if (keep) eff[ob + kept + __popc(km & lt_mask)] = us[q];
+        if (keep) {
+          const uint64_t r = kept + __popc(km & lt_mask);
+          eff[ob + r] = us[q];
+          if (SLAB && r < kSlab) eff[(uint64_t)v * kSlab + r] = us[q];
+        }
         kept += __popc(km);
       }
     }
-    if (lane == 0) edesc[v] = make_desc(ob, kept);
+    // (SLAB: a big vertex whose list fits its slab is read from the slab)
+    if (lane == 0) edesc[v] = (SLAB && kept <= kSlab) ? make_desc((uint64_t)v * kSlab, kept) : make_desc(ob, kept);
   }
 }
 
@@ -893,6 +933,26 @@ static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
   g_launches += 2;
 }
 
+// One pass into the slab layout: n slabs of kSlab slots, then the region of
+// the lists longer than a slab (big vertices and the g.slab_extra slots of
+// the others, both sized by degree).
+template <bool CODED>
+static void orient_slab(const DevGraph& g, DevEff& out, cudaStream_t s) {
+  const uint64_t ntiles = (g.n + 31) / 32;
+  const unsigned grid = grid_for(ntiles, kOWarps, 148u * kOBlocks);  // resident
+  DBuf<uint32_t> bigq(g.n, s);
+  DBuf<unsigned long long> ctr(6, s);
+  ctr.zero();
+  k_orient_tiles<2, CODED, true><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p,
+                                                               g.n, nullptr, out.desc.p, out.data.p,
+                                                               ctr.p, bigq.p, ctr.p + 1, nullptr, nullptr);
+  TG_CHECK_LAUNCH();
+  k_orient_big1<CODED, true><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq.p,
+                                                     g.n, ctr.p, g.n * kSlab, out.desc.p, out.data.p);
+  TG_CHECK_LAUNCH();
+  g_launches += 2;
+}
+
 // ---- chunked one-pass orientation (host CSR streamed in vertex chunks) ----
 //
 // The tile layout is position-independent (each tile writes inside its own
@@ -1100,8 +1160,10 @@ void select_ready(const uint8_t* ready, uint32_t vb, uint32_t ve, uint32_t k, ui
 //    lists back to back.
 void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   TG_REQUIRE(g.m2 < (1ull << 40), "graph too large for 40-bit list descriptors");
-  const uint64_t slots = g.m2 + g.big_entries;
-  if (!g.n || slots + kQuadPad >= (1ull << 34) || (g_orient_mode & 3) == 1)
+  const bool slab = g.slab && g.n && g.n * kSlab + g.big_entries + g.slab_extra + kQuadPad < (1ull << 34);
+  const uint64_t slots = slab ? g.n * kSlab + g.big_entries + g.slab_extra : g.m2 + g.big_entries;
+  out.slab = 0;
+  if (!g.n || slots + kQuadPad >= (1ull << 34) || (!slab && (g_orient_mode & 3) == 1))
     return orient_full_compact(g, out, s);
   out.rows = g.n;
   out.base = 0;
@@ -1110,6 +1172,12 @@ void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   if (out.desc.n < g.n) out.desc.alloc(g.n, s);
   if (out.data.n < slots + kQuadPad) out.data.alloc(slots + kQuadPad, s);
   out.off.release();
+  if (slab) {
+    out.slab = kSlab;
+    if (order_coded(g)) orient_slab<true>(g, out, s);
+    else orient_slab<false>(g, out, s);
+    return;
+  }
   if (order_coded(g)) orient_onepass<true>(g, out, s);
   else orient_onepass<false>(g, out, s);
 }
@@ -1211,6 +1279,47 @@ uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s) {
   TG_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
   TG_CUDA(cudaStreamSynchronize(s));
   return h;
+}
+
+// acc[0] = entries of the lists longer than a slab, acc[1] = degrees of their
+// vertices that the orientation does not treat as big, acc[2] = max h
+__global__ void k_slab_stats(const uint64_t* __restrict__ desc, const uint32_t* __restrict__ deg,
+                             uint64_t rows, unsigned long long* __restrict__ acc) {
+  unsigned long long a = 0, b = 0, mx = 0;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = desc_len(desc[r]);
+    if (h > kSlab) {
+      a += h;
+      if (deg[r] <= kOBig) b += deg[r];
+    }
+    mx = h > mx ? h : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(acc, a);
+    if (b) atomicAdd(acc + 1, b);
+    atomicMax(acc + 2, mx);
+  }
+}
+
+SlabStats slab_stats(const DevGraph& g, const DevEff& e, cudaStream_t s) {
+  DBuf<unsigned long long> acc(3, s);
+  acc.zero();
+  if (e.rows) {
+    k_slab_stats<<<grid_for(e.rows, 256, 148u * 8u), 256, 0, s>>>(e.desc.p, g.deg.p, e.rows, acc.p);
+    TG_CHECK_LAUNCH();
+    ++g_launches;
+  }
+  unsigned long long h[3] = {0, 0, 0};
+  TG_CUDA(cudaMemcpyAsync(h, acc.p, 24, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  return SlabStats{h[0], h[1], (uint32_t)h[2]};
 }
 
 uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s) {

@@ -92,7 +92,17 @@ struct DevGraph {
   int order = TG_ORDER_BY_DEGREE;
   uint64_t order_seed = 0;
   DBuf<uint32_t> okey;     // n (non-degree orders only)
+  // Slab layout of the oriented lists (orient_full): on when slab != 0;
+  // slab_extra = sum of the degrees of the vertices with h_v > kSlab that the
+  // orientation does not treat as big (the slots their full lists reserve).
+  uint32_t slab = 0;
+  uint64_t slab_extra = 0;
 };
+
+// Slab layout: list v in the 32 slots (one 128-byte DRAM line) at 32 v,
+// padded with kNoEntry (never a NodeId: n < 2^32 - 1 is required).
+constexpr uint32_t kSlab = 32;
+constexpr uint32_t kNoEntry = 0xffffffffu;
 
 extern int g_orient_mode;  // (see below)
 
@@ -138,10 +148,15 @@ __host__ __device__ __forceinline__ uint64_t make_desc(uint64_t start, uint64_t 
 //    and the exported EffectiveAdjacency;
 //  * gappy    -- N_v in the first h_v slots of v's symmetric-CSR slot range
 //    (start = sym_off[v]); built in ONE pass over the adjacency (the hot path).
+//  * slab     -- (slab = kSlab) the first min(h_v, 32) entries of N_v in the
+//    128-byte-aligned slab data[32 v, 32 v + 32), kNoEntry-padded, so a random
+//    list read is ONE DRAM line and needs no descriptor; lists longer than a
+//    slab are stored whole above the slabs (desc points there).
 struct DevEff {
   uint64_t rows = 0, entries = 0;
   uint32_t base = 0;
   bool compact = false;
+  uint32_t slab = 0;
   DBuf<uint64_t> desc;  // rows
   DBuf<uint64_t> off;   // rows+1 (compact layout only)
   DBuf<uint32_t> data;
@@ -158,6 +173,7 @@ struct CsrView {
   uint32_t base;
   float avg_len = 0.f;  // host-side hint: mean list length (kernel choice)
   bool quad_ok = false;  // host-side: list slots < 2^34 (32-bit quad indices)
+  uint32_t slab = 0;     // slab layout (DevEff::slab): list v also at data + 32 (v - base)
 };
 
 // ---- build / orient (build.cu, orient.cu) ----
@@ -191,6 +207,15 @@ void select_ready(const uint8_t* ready, uint32_t vb, uint32_t ve, uint32_t k, ui
 void eff_desc_from_off(DevEff& e, cudaStream_t s);
 // Compact copy of a (gappy) oriented CSR: off (n+1) and data (m).
 void compact_eff(const DevEff& in, DevEff& out, cudaStream_t s);
+// What the slab layout would cost for the oriented lists e of g (host result,
+// one sync): entries of the lists longer than a slab, the extra slots their
+// full copies reserve (DevGraph::slab_extra), the longest list.
+struct SlabStats {
+  uint64_t long_entries, extra_slots;
+  uint32_t max_len;
+};
+SlabStats slab_stats(const DevGraph& g, const DevEff& e, cudaStream_t s);
+extern int g_slab_mode;  // 0 auto, 1 force on, 2 off (tests, A/B)
 // sum of the lengths of the lists longer than thr (host result).
 uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s);
 // sum of list lengths over rows [lo, hi) (host result).
