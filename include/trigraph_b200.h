@@ -388,6 +388,7 @@ void tg_debug_set_rank_bitmap(int32_t mode, uint32_t cap_bits);
 /* Test hook: the large-graph code paths on small graphs.  orient_mode: 0
  * auto, 1 compact count/scan/fill orientation (taken above 2^34 list
  * slots), +4 = 1-byte degree codes as orientation keys (taken above 32M
+ * vertices), +8 = 4-bit endpoint-quantile degree codes (taken above 64M
  * vertices); force_wide: 64-bit element indices in the scalar
  * intersection kernels (taken above 2^32 list slots).  All exact. */
 void tg_debug_set_paths(int32_t orient_mode, int32_t force_wide);

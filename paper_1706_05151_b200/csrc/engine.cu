@@ -145,6 +145,7 @@ void orient(tg_graph* g) {
     g->slab_mode = -1;
     g->g.slab = 0;
   }
+  if (tgb::order_nibble_wanted(g->g) && g->g.nibble == 0) tgb::build_nibble_codes(g->g, g->stream);
   tgb::orient_full(g->g, g->eff, g->stream);
   if (g->slab_mode < 0) {
     g->slab_for = tgb::g_slab_mode;

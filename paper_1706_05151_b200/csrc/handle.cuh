@@ -49,7 +49,7 @@ struct tg_graph {
   // re-home stream-ordered frees when the caller switches streams)
   template <class F>
   void for_each_buf(F&& f) {
-    f(g.off); f(g.adj); f(g.deg); f(g.dcode); f(g.okey);
+    f(g.off); f(g.adj); f(g.deg); f(g.dcode); f(g.dcode4); f(g.okey);
     f(eff.off); f(eff.data); f(eff.desc); f(rk); f(rdata);
     f(win.rec); f(win.far); f(win.ctr); f(wdefer);
     f(scr.big); f(scr.big_count);

@@ -429,7 +429,7 @@ void launch_warp(const Apex& A, uint64_t items, CsrView nu, uint32_t ulo, uint32
       const unsigned wgrid = grid_for(items, kWarpsPerBlock, 148u * kSlabBlocks);  // resident
       uint64_t chunk = items / ((uint64_t)wgrid * kWarpsPerBlock * 16);
       chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
-      k_intersect_slab<TALLY, LIST, FILTER, Apex><<<wgrid, kWarpsPerBlock * 32, 0, s>>>(
+      k_intersect_slab<TALLY, LIST, FILTER, Apex><<<wgrid, kWarpsPerBlock * 32, kSlabSmem, s>>>(
           A, nu, ulo, uhi, out, scr.big.p, scr.big_count.p, scr.big.n, scr.big_count.p + 2,
           (uint32_t)chunk);
       TG_CHECK_LAUNCH();

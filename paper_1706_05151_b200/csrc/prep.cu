@@ -119,16 +119,41 @@ __device__ __forceinline__ bool precedes_coded(uint8_t cv, uint32_t v, uint8_t c
   return dv < du || (dv == du && v < u);
 }
 
-// Order key of a vertex: its degree, or its 1-byte code when the degree array
-// would not stay L2-resident (n beyond ~32M vertices).
-template <bool CODED>
+// Order key of a vertex.  CODED 0: its degree; 1: its 1-byte code, when the
+// degree array would not stay L2-resident (n beyond ~32M vertices); 2: a
+// 4-bit code (two per byte) when even the 1-byte codes would not (n beyond
+// ~64M: ncu of the C5 orientation showed 114 of its 131 GB of DRAM reads
+// were 128-byte line fills for 1-byte lookups in the 100 MB code table).
+// The 16 codes are degree buckets of equal ENDPOINT mass (build_nibble_codes),
+// so a random edge's ends rarely share one; a tie inside a bucket that holds
+// a single degree (bit of xmask) is decided by the ids, any other by the
+// exact degrees.  The apex's own key packs (code << 28) | degree.
+__device__ __forceinline__ uint32_t nibble_at(const uint8_t* __restrict__ t, uint32_t v) {
+  return ((uint32_t)__ldg(t + (v >> 1)) >> ((v & 1u) * 4u)) & 15u;
+}
+template <int CODED>
 __device__ __forceinline__ uint32_t okey(const uint32_t* __restrict__ deg,
                                          const uint8_t* __restrict__ dcode, uint32_t v) {
+  if (CODED == 2) return (nibble_at(dcode, v) << 28) | __ldg(deg + v);
   return CODED ? (uint32_t)__ldg(dcode + v) : __ldg(deg + v);
 }
-template <bool CODED>
+// key of a neighbour (the random lookups)
+template <int CODED>
+__device__ __forceinline__ uint32_t okey_nb(const uint32_t* __restrict__ deg,
+                                            const uint8_t* __restrict__ dcode, uint32_t u) {
+  if (CODED == 2) return nibble_at(dcode, u);
+  return okey<CODED>(deg, dcode, u);
+}
+template <int CODED>
 __device__ __forceinline__ bool okey_precedes(uint32_t kv, uint32_t v, uint32_t ku, uint32_t u,
-                                              const uint32_t* __restrict__ deg) {
+                                              const uint32_t* __restrict__ deg, uint32_t xmask = 0) {
+  if (CODED == 2) {
+    const uint32_t cv = kv >> 28;
+    if (cv != ku) return cv < ku;
+    if ((xmask >> cv) & 1u) return v < u;  // one degree in the bucket: tie broken by id
+    const uint32_t dv = kv & 0x0FFFFFFFu, du = __ldg(deg + u);
+    return dv < du || (dv == du && v < u);
+  }
   return CODED ? precedes_coded((uint8_t)kv, v, (uint8_t)ku, u, deg) : precedes(kv, v, ku, u);
 }
 
@@ -252,7 +277,7 @@ constexpr uint32_t kOHub = 4096;  // ... and above which a whole CTA orients it 
 //          in the 32-slot, 128-byte-aligned slab eff[32v, 32v+32), kNoEntry
 //          padded; vertices with h_v > 32 are re-oriented by k_orient_big1
 //          (full list above the slabs, its first 32 entries in the slab).
-template <int MODE, bool CODED, bool SLAB = false>
+template <int MODE, int CODED, bool SLAB = false>
 __global__ void __launch_bounds__(kOWarps * 32, kOBlocks)
 k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode, uint64_t n,
@@ -261,7 +286,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
                unsigned long long* __restrict__ tile_ctr, uint32_t* __restrict__ bigq,
                unsigned long long* __restrict__ bigq_n, uint32_t* __restrict__ kmask,
                const uint64_t* __restrict__ hcnt, uint64_t tile_lo = 0,
-               uint64_t tile_hi = ~0ull) {
+               uint64_t tile_hi = ~0ull, uint32_t xmask = 0) {
   __shared__ uint32_t sTbl[kOWarps][kOTbl + kOUnroll];
   __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
   __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
@@ -400,7 +425,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
           uint32_t dus[kOUnroll];
 #pragma unroll
           for (int q = 0; q < kOUnroll; ++q)
-            dus[q] = (base0 + 32 * q + lane < wend) ? okey<CODED>(deg, dcode, us[q]) : 0u;
+            dus[q] = (base0 + 32 * q + lane < wend) ? okey_nb<CODED>(deg, dcode, us[q]) : 0u;
 #pragma unroll
           for (int q = 0; q < kOUnroll; ++q) {
             const uint32_t base = base0 + 32 * q;
@@ -408,7 +433,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
             const uint32_t jj = jjs[q];
             const uint32_t sv = __shfl_sync(FULL, c_v, jj);
             const uint32_t sdv = __shfl_sync(FULL, c_dv, jj);
-            const bool keep = idx < wend && okey_precedes<CODED>(sdv, sv, dus[q], us[q], deg);
+            const bool keep = idx < wend && okey_precedes<CODED>(sdv, sv, dus[q], us[q], deg, xmask);
             const unsigned km = __ballot_sync(FULL, keep);
             const uint32_t send = __shfl_sync(FULL, c_end, jj);
             if (idx < wend && idx + 1 == send) sCum[w][jj] = kept + __popc(km & le_mask);
@@ -455,7 +480,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
 
 // Big vertices: 32 lanes per vertex over a device-side queue.  COUNT writes
 // h_v; FILL writes N_v at eoff[v] in adjacency order (ballot prefix).
-template <bool FILL, bool CODED>
+template <bool FILL, int CODED>
 __global__ void __launch_bounds__(256)
 k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
              const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode,
@@ -494,7 +519,7 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
       } else {
         u1 = k1 < e ? __ldcs(adj + k1) : 0u;
         u2 = k2 < e ? __ldcs(adj + k2) : 0u;
-        const uint32_t c1 = k1 < e ? okey<CODED>(deg, dcode, u1) : 0, c2 = k2 < e ? okey<CODED>(deg, dcode, u2) : 0;
+        const uint32_t c1 = k1 < e ? okey_nb<CODED>(deg, dcode, u1) : 0, c2 = k2 < e ? okey_nb<CODED>(deg, dcode, u2) : 0;
         const bool p1 = k1 < e && okey_precedes<CODED>(cv, v, c1, u1, deg);
         const bool p2 = k2 < e && okey_precedes<CODED>(cv, v, c2, u2, deg);
         m1 = __ballot_sync(0xffffffffu, p1);
@@ -531,12 +556,13 @@ k_orient_big(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
 constexpr int kBigU = 4;
 // SLAB: the first kSlab kept entries also go to v's slab (padded by the tile
 // kernel), and the queue holds the non-big vertices with h_v > kSlab too.
-template <bool CODED, bool SLAB = false>
+template <int CODED, bool SLAB = false>
 __global__ void __launch_bounds__(256)
 k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
               const uint32_t* __restrict__ deg, const uint8_t* __restrict__ dcode,
               const uint32_t* __restrict__ bigq, uint64_t n, unsigned long long* __restrict__ c,
-              uint64_t m2, uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff) {
+              uint64_t m2, uint64_t* __restrict__ edesc, uint32_t* __restrict__ eff,
+              uint32_t xmask = 0) {
   __shared__ uint32_t sM[256], sO[256], sW[8];
   __shared__ unsigned long long sI, sBase;
   const unsigned t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -565,11 +591,11 @@ k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj
         }
 #pragma unroll
         for (int q = 0; q < kBigU; ++q)
-          ks[q] = (wb + 32 * (ch0 + q) + lane < e) ? okey<CODED>(deg, dcode, us[q]) : 0u;
+          ks[q] = (wb + 32 * (ch0 + q) + lane < e) ? okey_nb<CODED>(deg, dcode, us[q]) : 0u;
 #pragma unroll
         for (int q = 0; q < kBigU; ++q) {
           const bool keep =
-              wb + 32 * (ch0 + q) + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg);
+              wb + 32 * (ch0 + q) + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg, xmask);
           const unsigned km = __ballot_sync(FULL, keep);
           if (lane == 0) sM[32 * w + ch0 + q] = km;
         }
@@ -631,11 +657,11 @@ k_orient_big1(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj
       }
 #pragma unroll
       for (int q = 0; q < kBigU; ++q)
-        ks[q] = (k0 + 32 * q + lane < e) ? okey<CODED>(deg, dcode, us[q]) : 0u;
+        ks[q] = (k0 + 32 * q + lane < e) ? okey_nb<CODED>(deg, dcode, us[q]) : 0u;
 #pragma unroll
       for (int q = 0; q < kBigU; ++q) {
         const bool keep =
-            k0 + 32 * q + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg);
+            k0 + 32 * q + lane < e && okey_precedes<CODED>(cv, v, ks[q], us[q], deg, xmask);
         const unsigned km = __ballot_sync(FULL, keep);
         if (keep) {
           const uint64_t r = kept + __popc(km & lt_mask);
@@ -852,6 +878,106 @@ void compute_degrees(DevGraph& g, cudaStream_t s) {
   }
 }
 
+// ---- 4-bit order codes (okey<2>) ----
+// histogram of min(degree, 65535) (block-private for degrees < 2048), the
+// degree mass of the clipped bin and the maximum degree
+constexpr uint32_t kHistBins = 65536, kHistSmem = 2048;
+__global__ void __launch_bounds__(256)
+k_deg_hist(const uint32_t* __restrict__ deg, uint64_t n, unsigned long long* __restrict__ hist,
+           unsigned long long* __restrict__ top /* [0] clipped mass, [1] max degree */) {
+  __shared__ uint32_t sh[kHistSmem];
+  for (uint32_t i = threadIdx.x; i < kHistSmem; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  unsigned long long mx = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = deg[v];
+    mx = d > mx ? d : mx;
+    if (d < kHistSmem) atomicAdd(&sh[d], 1u);
+    else if (d < kHistBins - 1) atomicAdd(&hist[d], 1ull);
+    else {
+      atomicAdd(&hist[kHistBins - 1], 1ull);
+      atomicAdd(top, (unsigned long long)d);
+    }
+  }
+  atomicMax(top + 1, mx);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kHistSmem; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+struct NibbleThr {
+  uint32_t t[16];  // code(d) = #{c in 1..15 : d >= t[c]}
+};
+__global__ void k_nibble_codes(const uint32_t* __restrict__ deg, uint64_t n, NibbleThr thr,
+                               uint32_t* __restrict__ words) {
+  // a thread packs the codes of 8 consecutive vertices into one word
+  for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi * 8 < n;
+       wi += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint64_t v = wi * 8 + i;
+      uint32_t c = 0;
+      if (v < n) {
+        const uint32_t d = deg[v];
+#pragma unroll
+        for (int k = 1; k < 16; ++k) c += d >= thr.t[k];
+      }
+      word |= c << (4 * i);
+    }
+    words[wi] = word;
+  }
+}
+
+void build_nibble_codes(DevGraph& g, cudaStream_t s) {
+  g.nibble = -1;
+  if (!g.n) return;
+  DBuf<unsigned long long> hist(kHistBins + 2, s);
+  hist.zero();
+  k_deg_hist<<<148 * 8, 256, 0, s>>>(g.deg.p, g.n, hist.p, hist.p + kHistBins);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+  std::vector<unsigned long long> h(kHistBins + 2);
+  TG_CUDA(cudaMemcpyAsync(h.data(), hist.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+  TG_CUDA(cudaStreamSynchronize(s));
+  if (h[kHistBins + 1] >= (1ull << 28)) return;  // the packed apex key holds 28 degree bits
+  // 16 buckets of equal endpoint mass: code(d) = floor(16 cum(d) / total)
+  long double total = (long double)h[kHistBins];
+  for (uint32_t d = 0; d + 1 < kHistBins; ++d) total += (long double)h[d] * d;
+  if (total <= 0) return;
+  NibbleThr thr;
+  for (int k = 0; k < 16; ++k) thr.t[k] = 0xffffffffu;
+  thr.t[0] = 0;
+  long double cum = 0;
+  uint32_t prev = 0;
+  for (uint32_t d = 0; d < kHistBins; ++d) {
+    cum += d + 1 < kHistBins ? (long double)h[d] * d : (long double)h[kHistBins];
+    uint32_t c = (uint32_t)(16.0L * cum / total);
+    c = c > 15 ? 15 : c;
+    if (!h[d]) continue;
+    for (uint32_t k = prev + 1; k <= c; ++k) thr.t[k] = d;  // first degree with code >= k
+    prev = c > prev ? c : prev;
+  }
+  // buckets holding exactly one degree value (the clipped bin never does)
+  uint32_t xmask = 0;
+  for (uint32_t k = 0; k < 16; ++k) {
+    const uint64_t lo = thr.t[k], hi = k < 15 ? thr.t[k + 1] : 0xffffffffull;
+    if (lo == 0xffffffffu) continue;
+    uint64_t distinct = 0;
+    for (uint64_t d = lo; d < hi && d < kHistBins && distinct < 2; ++d) distinct += h[d] != 0;
+    if (hi >= kHistBins - 1) distinct = 2;
+    if (distinct <= 1) xmask |= 1u << k;
+  }
+  const uint64_t words = (g.n + 7) / 8;
+  g.dcode4.alloc(words * 4, s);
+  k_nibble_codes<<<grid_for(words, 256), 256, 0, s>>>(g.deg.p, g.n, thr, (uint32_t*)g.dcode4.p);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+  g.xmask = xmask;
+  g.nibble = 1;
+}
+
 // effective.hpp:37-52 for rows [vlo, vhi), compact layout (partitions, the
 // exported EffectiveAdjacency).  One host sync for the entry count.
 void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cudaStream_t s) {
@@ -883,7 +1009,7 @@ void orient_rows(const DevGraph& g, uint32_t vlo, uint32_t vhi, DevEff& out, cud
   out.entries = entries;
 }
 
-template <bool CODED>
+template <int CODED>
 static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t ntiles = (g.n + 31) / 32;
   const unsigned grid = grid_for(ntiles, kOWarps, 148u * kOBlocks);  // resident
@@ -916,19 +1042,21 @@ static void orient_tiles(const DevGraph& g, DevEff& out, cudaStream_t s) {
   g_launches += 6;  // count, big count, scan (init + sweep), fill, big fill
 }
 
-template <bool CODED>
+template <int CODED>
 static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t ntiles = (g.n + 31) / 32;
   const unsigned grid = grid_for(ntiles, kOWarps, 148u * kOBlocks);  // resident
   DBuf<uint32_t> bigq(g.n, s);
   DBuf<unsigned long long> ctr(6, s);  // tile counter + k_orient_big1's counters
   ctr.zero();
-  k_orient_tiles<2, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, g.n,
+  const uint8_t* codes = CODED == 2 ? g.dcode4.p : g.dcode.p;
+  k_orient_tiles<2, CODED><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), codes, g.n,
                                                          nullptr, out.desc.p, out.data.p, ctr.p,
-                                                         bigq.p, ctr.p + 1, nullptr, nullptr);
+                                                         bigq.p, ctr.p + 1, nullptr, nullptr, 0,
+                                                         ~0ull, g.xmask);
   TG_CHECK_LAUNCH();
-  k_orient_big1<CODED><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq.p, g.n,
-                                               ctr.p, g.m2, out.desc.p, out.data.p);
+  k_orient_big1<CODED><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), codes, bigq.p, g.n,
+                                               ctr.p, g.m2, out.desc.p, out.data.p, g.xmask);
   TG_CHECK_LAUNCH();
   g_launches += 2;
 }
@@ -936,19 +1064,22 @@ static void orient_onepass(const DevGraph& g, DevEff& out, cudaStream_t s) {
 // One pass into the slab layout: n slabs of kSlab slots, then the region of
 // the lists longer than a slab (big vertices and the g.slab_extra slots of
 // the others, both sized by degree).
-template <bool CODED>
+template <int CODED>
 static void orient_slab(const DevGraph& g, DevEff& out, cudaStream_t s) {
   const uint64_t ntiles = (g.n + 31) / 32;
   const unsigned grid = grid_for(ntiles, kOWarps, 148u * kOBlocks);  // resident
   DBuf<uint32_t> bigq(g.n, s);
   DBuf<unsigned long long> ctr(6, s);
   ctr.zero();
-  k_orient_tiles<2, CODED, true><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p,
+  const uint8_t* codes = CODED == 2 ? g.dcode4.p : g.dcode.p;
+  k_orient_tiles<2, CODED, true><<<grid, kOWarps * 32, 0, s>>>(g.off.p, g.adj.p, order_key(g), codes,
                                                                g.n, nullptr, out.desc.p, out.data.p,
-                                                               ctr.p, bigq.p, ctr.p + 1, nullptr, nullptr);
+                                                               ctr.p, bigq.p, ctr.p + 1, nullptr, nullptr,
+                                                               0, ~0ull, g.xmask);
   TG_CHECK_LAUNCH();
-  k_orient_big1<CODED, true><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), g.dcode.p, bigq.p,
-                                                     g.n, ctr.p, g.n * kSlab, out.desc.p, out.data.p);
+  k_orient_big1<CODED, true><<<148 * 6, 256, 0, s>>>(g.off.p, g.adj.p, order_key(g), codes, bigq.p,
+                                                     g.n, ctr.p, g.n * kSlab, out.desc.p, out.data.p,
+                                                     g.xmask);
   TG_CHECK_LAUNCH();
   g_launches += 2;
 }
@@ -1174,12 +1305,14 @@ void orient_full(const DevGraph& g, DevEff& out, cudaStream_t s) {
   out.off.release();
   if (slab) {
     out.slab = kSlab;
-    if (order_coded(g)) orient_slab<true>(g, out, s);
-    else orient_slab<false>(g, out, s);
+    if (order_nibble(g)) orient_slab<2>(g, out, s);
+    else if (order_coded(g)) orient_slab<1>(g, out, s);
+    else orient_slab<0>(g, out, s);
     return;
   }
-  if (order_coded(g)) orient_onepass<true>(g, out, s);
-  else orient_onepass<false>(g, out, s);
+  if (order_nibble(g)) orient_onepass<2>(g, out, s);
+  else if (order_coded(g)) orient_onepass<1>(g, out, s);
+  else orient_onepass<0>(g, out, s);
 }
 
 // count -> CUB scan -> fill, compact layout (sum h_v = m is known).

@@ -85,6 +85,11 @@ struct DevGraph {
   DBuf<uint32_t> adj;      // m2
   DBuf<uint32_t> deg;      // n
   DBuf<uint8_t> dcode;     // n: monotone 1-byte degree code (orientation)
+  // 4-bit degree codes, two per byte (build_nibble_codes): nibble 0 not
+  // built yet, 1 built, -1 not applicable; xmask = buckets of one degree
+  DBuf<uint8_t> dcode4;
+  int nibble = 0;
+  uint32_t xmask = 0;
   uint64_t big_entries = 0;  // sum of degrees of the orientation's hub vertices
   // Total order of the orientation (order.hpp:17-35).  ByDegree keys on
   // `deg` (or `dcode`); every other kind keys on okey = its rank array, so
@@ -118,6 +123,17 @@ inline bool order_coded(const DevGraph& g) {
   return g.order == TG_ORDER_BY_DEGREE &&
          (g.n > (uint64_t)(TG_CODED_MIN_N) || (g_orient_mode & 4));
 }
+
+// 4-bit codes once even the 1-byte codes would not stay in L2 (the full
+// orientation only; built by build_nibble_codes on first use).
+#ifndef TG_NIBBLE_MIN_N
+#define TG_NIBBLE_MIN_N (64ull << 20)
+#endif
+inline bool order_nibble_wanted(const DevGraph& g) {
+  return g.order == TG_ORDER_BY_DEGREE && (g.n > (uint64_t)(TG_NIBBLE_MIN_N) || (g_orient_mode & 8));
+}
+inline bool order_nibble(const DevGraph& g) { return order_nibble_wanted(g) && g.nibble == 1; }
+void build_nibble_codes(DevGraph& g, cudaStream_t s);
 
 // Monotone 1-byte code of a degree: exact below 240, then one bucket per
 // doubling.  code(a) < code(b) implies a < b; equal codes below 240 imply

@@ -1,6 +1,7 @@
 """The code paths large graphs take, forced on small ones (tg_debug_set_paths):
 compact count/scan/fill orientation (above 2^34 list slots, effective.hpp:37-52),
-1-byte degree codes as orientation keys (above 32M vertices, order.hpp:95-104)
+1-byte degree codes as orientation keys (above 32M vertices, order.hpp:95-104),
+4-bit endpoint-quantile degree codes (+8, above 64M vertices)
 and 64-bit element indices in the scalar intersection kernels (above 2^32
 slots, sequential.hpp:74-91) -- each bit-exact against the oracle for counts,
 per-node tallies, listings and per-rank engine results."""
@@ -28,7 +29,8 @@ GRAPHS = {
 
 @pytest.mark.parametrize("graph", sorted(GRAPHS))
 @pytest.mark.parametrize("orient_mode,force_wide,variant", [
-    (1, 0, 0), (5, 0, 0), (6, 0, 0), (1, 1, 1), (1, 1, 4), (6, 1, 1), (2, 1, 4)])
+    (1, 0, 0), (5, 0, 0), (6, 0, 0), (1, 1, 1), (1, 1, 4), (6, 1, 1), (2, 1, 4),
+    (8, 0, 0), (10, 0, 0)])
 def test_forced_large_graph_paths(graph, orient_mode, force_wide, variant):
     pairs = GRAPHS[graph]()
     ref = O.build_graph(pairs)

@@ -97,6 +97,25 @@ def test_slab_matches_oracle(slab, graph, mode):
     g.close()
 
 
+@pytest.mark.parametrize("graph", ["pa", "rmat", "hub_clique", "random"])
+def test_slab_with_nibble_codes(slab, graph):
+    """the slab orientation keyed by the 4-bit degree codes (n > 64M path)"""
+    pairs = GRAPHS[graph]()
+    ref = O.build_graph(pairs)
+    want = O.count(ref)[0]
+    eoff, eadj = O.effective(ref)
+    try:
+        slab.tg_debug_set_paths(8, 0)
+        slab.tg_debug_set_slab(1)
+        g = T.build_graph(pairs, ref.n)
+        e = T.effective_adjacency(g)
+        assert np.array_equal(e.offsets, eoff) and np.array_equal(e.entries, eadj)
+        assert T.count_node_iterator_n(g) == want
+        g.close()
+    finally:
+        slab.tg_debug_set_paths(0, 0)
+
+
 def test_slab_quad_kernel_on_slab_layout(slab):
     """the descriptor-driven kernels read the slab layout too (variant sweep)"""
     pairs = T.gen_pa(20000, 50, 11)
