@@ -260,10 +260,10 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint64_t n, uint64_
 }
 
 __global__ void k_desc_from_off2(const uint64_t* __restrict__ off, uint64_t rows,
-                                 uint64_t* __restrict__ desc) {
+                                 uint64_t* __restrict__ desc, uint64_t shift = 0) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
        r += (uint64_t)gridDim.x * blockDim.x)
-    desc[r] = make_desc(off[r], off[r + 1] - off[r]);
+    desc[r] = make_desc(shift + off[r], off[r + 1] - off[r]);
 }
 
 __global__ void k_dcode(const uint32_t* __restrict__ deg, uint64_t n, uint8_t* __restrict__ dcode) {
@@ -719,11 +719,6 @@ tg_status tg_aop_step_comm(tg_graph* g, tg_comm* c, const uint32_t* boundaries, 
     full.base = 0;
     full.compact = true;
     full.entries = m;
-    full.data.alloc(m + tgb::kQuadPad, s);
-    TG_CUDA(cudaMemsetAsync(full.data.p + m, 0, tgb::kQuadPad * 4, s));
-    if (o.slice.entries)
-      TG_CUDA(cudaMemcpyAsync(full.data.p + base[r], o.slice.data.p, o.slice.entries * 4,
-                              cudaMemcpyDeviceToDevice, s));
     offsets_from_lens(o.lens, n, full.off, s);
     full.desc.alloc(n ? n : 1, s);
     if (n) {
@@ -731,6 +726,32 @@ tg_status tg_aop_step_comm(tg_graph* g, tg_comm* c, const uint32_t* boundaries, 
       TG_CHECK_LAUNCH();
       ++tgb::g_launches;
     }
+    // Slab layout for the count (slab.cuh) when the gathered lists suit it
+    // (the rule of engine.cu orient, decided once per order): the lists are
+    // received behind the n slabs and each slice's slabs are filled on
+    // arrival (one streaming pass over the slice, under the next transfer).
+    if (g->comm_slab < 0) {
+      g->comm_slab = 0;
+      const int mode = tgb::g_slab_mode & 255;
+      if (mode != 2 && n && n < 0xffffffffull) {
+        const tgb::SlabStats st = tgb::slab_stats(g->g, full, s);
+        const bool fits = n * tgb::kSlab + m + tgb::kQuadPad < (1ull << 34);
+        const bool pays = m > 16 * n && st.long_entries * 50 <= m && st.max_len <= 4096;
+        if (fits && (pays || mode == 1)) g->comm_slab = 1;
+      }
+    }
+    const uint64_t lb = g->comm_slab == 1 ? n * tgb::kSlab : 0;  // first list slot
+    if (lb) {
+      full.slab = tgb::kSlab;
+      tgb::k_desc_from_off2<<<tgb::grid_for(n, 256), 256, 0, s>>>(full.off.p, n, full.desc.p, lb);
+      TG_CHECK_LAUNCH();
+      ++tgb::g_launches;
+    }
+    full.data.alloc(lb + m + tgb::kQuadPad, s);
+    TG_CUDA(cudaMemsetAsync(full.data.p + lb + m, 0, tgb::kQuadPad * 4, s));
+    if (o.slice.entries)
+      TG_CUDA(cudaMemcpyAsync(full.data.p + lb + base[r], o.slice.data.p, o.slice.entries * 4,
+                              cudaMemcpyDeviceToDevice, s));
     // the slices arrive in rank order (= id order) on a transfer stream; after
     // slice k, every apex of this rank's core whose lists all arrived --
     // ready chunk max(chunk(v), chunk(last of N_v)), lists being ID-sorted --
@@ -752,9 +773,10 @@ tg_status tg_aop_step_comm(tg_graph* g, tg_comm* c, const uint32_t* boundaries, 
     const CsrView fv = tgh::view(full);
     try {
       for (int k = 0; k < N; ++k) {
-        T.broadcast(full.data.p + base[k], o.cnt[k] * 4, k, xs);
+        T.broadcast(full.data.p + lb + base[k], o.cnt[k] * 4, k, xs);
         TG_CUDA(cudaEventRecord(ev_x, xs));
         TG_CUDA(cudaStreamWaitEvent(s, ev_x, 0));
+        if (lb) tgb::slab_rows(full, o.a[k], o.a[k + 1], s);
         const uint32_t vb = std::max(o.a[k], cb), ve = std::min(o.a[k + 1], ce);
         tgb::ready_chunks(full, d_a.p, (uint32_t)N, (uint32_t)k, vb, ve, ready.p, s);
         if (ce > cb) {

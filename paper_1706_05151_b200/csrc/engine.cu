@@ -129,6 +129,7 @@ void apply_order(tg_graph* g, int kind, uint64_t seed) {
   g->rank_mode = -1;
   g->window_mode = -1;
   g->slab_mode = -1;
+  g->comm_slab = -1;
   g->g.slab = 0;
 }
 

@@ -24,6 +24,7 @@ struct tg_graph {
   // slab layout of the oriented lists: -1 undecided, 0 off, 1 on (per order;
   // decided under slab_for = the g_slab_mode in force)
   int slab_mode = -1, slab_for = 0;
+  int comm_slab = -1;  // the same choice for the gathered lists of tg_aop_step_comm
   // window encoding (window.cu): -1 undecided, 0 off, 1 on (per order)
   int window_mode = -1;
   uint64_t window_far = 0;

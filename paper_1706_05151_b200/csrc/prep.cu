@@ -1455,6 +1455,27 @@ SlabStats slab_stats(const DevGraph& g, const DevEff& e, cudaStream_t s) {
   return SlabStats{h[0], h[1], (uint32_t)h[2]};
 }
 
+// slabs of rows [vb, ve) from their lists (a warp per row: one coalesced
+// 128-byte store, pads past h_v)
+__global__ void __launch_bounds__(256)
+k_slab_rows(const uint64_t* __restrict__ desc, uint32_t* __restrict__ data, uint64_t vb, uint64_t ve) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = vb + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); v < ve; v += warps) {
+    const uint64_t d = desc[v];
+    const uint32_t h = desc_len(d);
+    const uint32_t x = lane < h ? __ldcs(data + desc_start(d) + lane) : kNoEntry;
+    data[v * kSlab + lane] = x;
+  }
+}
+
+void slab_rows(DevEff& e, uint32_t vb, uint32_t ve, cudaStream_t s) {
+  if (ve <= vb) return;
+  k_slab_rows<<<grid_for((uint64_t)(ve - vb) * 32, 256, 148u * 16u), 256, 0, s>>>(e.desc.p, e.data.p, vb, ve);
+  TG_CHECK_LAUNCH();
+  ++g_launches;
+}
+
 uint64_t sum_lens(const DevEff& e, uint32_t lo, uint32_t hi, cudaStream_t s) {
   DBuf<unsigned long long> acc(1, s);
   acc.zero();

@@ -20,6 +20,10 @@
 // that its <= 64 keys do not collide (a perfect hash: retry with the next
 // multiplier on a collision, 17% of the tries at h_v = 20).  A probe is then
 // IMAD, SHF, LOP3, LDS, ISETP -- exact, no filter, no second search.
+// (C5: 70 -> 54 ms.  Measured and dropped afterwards: skipping a round's empty
+// loads warp-uniformly, an all-pad slab for the lanes of a partial load and
+// folded 64-bit addresses -- the same time at 4 resident blocks per SM, 6%
+// slower at 5: the kernel now waits on DRAM lines, not on issue slots.)
 //
 // One warp per apex v (N_v = slab v, prefetched one apex ahead).  A warp load
 // reads 4 whole slabs (8 lanes x 16 bytes each); a round of 6 loads covers 24
@@ -31,7 +35,7 @@
 #define TG_SLAB_U 6
 #endif
 #ifndef TG_SLAB_BLOCKS
-#define TG_SLAB_BLOCKS 5
+#define TG_SLAB_BLOCKS 4
 #endif
 constexpr int kSlabU = TG_SLAB_U;            // warp loads per round (4 lists each)
 constexpr int kSlabBlocks = TG_SLAB_BLOCKS;  // resident blocks per SM

@@ -189,7 +189,7 @@ struct CsrView {
   uint32_t base;
   float avg_len = 0.f;  // host-side hint: mean list length (kernel choice)
   bool quad_ok = false;  // host-side: list slots < 2^34 (32-bit quad indices)
-  uint32_t slab = 0;     // slab layout (DevEff::slab): list v also at data + 32 (v - base)
+  uint32_t slab = 0;     // slab layout (DevEff::slab, base = 0): list v also at data + 32 v
 };
 
 // ---- build / orient (build.cu, orient.cu) ----
@@ -231,6 +231,9 @@ struct SlabStats {
   uint32_t max_len;
 };
 SlabStats slab_stats(const DevGraph& g, const DevEff& e, cudaStream_t s);
+// Fill the slabs of rows [vb, ve) of a slab-layout `e` (base 0) whose lists
+// were written elsewhere in e.data (gathered lists: desc points at them).
+void slab_rows(DevEff& e, uint32_t vb, uint32_t ve, cudaStream_t s);
 extern int g_slab_mode;  // 0 auto, 1 force on, 2 off (tests, A/B)
 // sum of the lengths of the lists longer than thr (host result).
 uint64_t heavy_entries(const DevEff& e, uint32_t thr, cudaStream_t s);

@@ -104,6 +104,39 @@ def test_engines_across_ranks(graph, nranks, local_rows):
         assert np.array_equal(cc, want_cc[lo:hi])
 
 
+@pytest.mark.parametrize("graph", ["pa", "rmat", "random"])
+@pytest.mark.parametrize("nranks", [1, 3])
+@pytest.mark.parametrize("slab_mode", [1, 2])
+def test_aop_step_slab_layout(graph, nranks, slab_mode):
+    """tg_aop_step_comm with the gathered lists in the slab layout (slab.cuh;
+    automatic on PA-like graphs, forced here) and without it"""
+    from paper_1706_05151_b200._lib import lib
+
+    pairs = GRAPHS[graph]() if graph != "pa" else T.gen_pa(20000, 44, 3)
+    ref = O.build_graph(pairs)
+    rows = M.split_rows(ref.off, nranks)
+    want = O.run_engine(ref, "aop", nranks, "DPD")
+
+    def body(r, comm):
+        g = rank_graph(ref, pairs, rows, r, True)
+        plan = M.run_engine_comm(g, comm, T.EngineConfig(engine=T.EngineKind.Aop)).boundaries
+        d = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = []
+        for _ in range(2):
+            M.aop_step_comm(g, comm, plan, d.data_ptr())
+            torch.cuda.synchronize()
+            out.append(int(d.item()))
+        g.close()
+        return out
+
+    try:
+        lib().tg_debug_set_slab(slab_mode)
+        for out in run_ranks(nranks, body):
+            assert out == [want.total, want.total]
+    finally:
+        lib().tg_debug_set_slab(0)
+
+
 def test_boundary_override_and_other_costs():
     pairs = GRAPHS["pa"]()
     ref = O.build_graph(pairs)
