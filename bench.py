@@ -539,7 +539,9 @@ def run_ours(args):
     traffic, traffic_src = profile_traffic(args.config)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "intersect pass (k_intersect_quad + the CTA / group kernels)",
+                "dram_gbs": (traffic / (isect_avg / 1e3) / 1e9) if traffic else None,
+                "kernel": "intersection pass (k_intersect_slab on the PA configs C2 / C5; the quad / "
+                          "group / window / CTA kernels otherwise)",
                 "algorithmic_bytes_per_pass": 4 * w_rank, "W": W,
                 "pass_ms": isect_avg, "orient_ms": orient_avg, "peak_source": peak_kind}
 

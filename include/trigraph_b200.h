@@ -312,7 +312,7 @@ tg_status tg_surrogate_count_device(tg_graph* g, const uint32_t* boundaries, uin
  * 211-268).  Every rank holds rows [lo, hi) of the symmetric CSR (the ranks'
  * ranges tile [0, n) in rank order) and the global degrees -- a graph from
  * tg_graph_from_rows -- or the whole graph (then its rows are an equal-
- * adjacency-volume split).  Each rank orients only its rows.  One C++ host
+ * orientation-cost split: adjacency entries + 32 per row).  Each rank orients only its rows.  One C++ host
  * can drive N devices: create the communicators, then call each rank's
  * entry points from its own host thread.  NCCL is loaded at run time. */
 typedef struct tg_comm tg_comm;
@@ -333,15 +333,23 @@ tg_status tg_comm_info(tg_comm* c, int32_t* nranks, int32_t* rank);
 tg_status tg_graph_from_rows(int device, uint64_t n, uint32_t row_lo, uint32_t row_hi,
                              const uint64_t* offsets, const uint32_t* adj,
                              const uint32_t* degrees, tg_graph** out);
-/* run_engine (engines.hpp:335-418) across the communicator, Aop or
- * AnopSurrogate, counts (no sinks, no sparsification, degree order):
+/* run_engine (engines.hpp:335-418) across the communicator, Aop,
+ * AnopDirect or AnopSurrogate, counts (no sinks, no sparsification, degree
+ * order):
  *  Aop       -- own rows oriented, the oriented rows gathered (one broadcast
  *               per rank), the cfg->cost plan from the gathered costs, the
  *               rank's core counted, one all-reduce of T;
  *  Surrogate -- own rows oriented, list lengths gathered, the plan from
  *               distributed costs, oriented rows moved to their core owner
  *               (one all-to-allv: Σ stored = m), the (v, N_v) messages
- *               exchanged (all-to-allv), SurrogateCount.
+ *               exchanged (all-to-allv), SurrogateCount;
+ *  Direct    -- (engines.hpp:80-141) the same core partitions; every
+ *               off-core pair (v, u) is one request to owner(u) and one reply
+ *               carrying N_u (no caching, as in the reference), batched into
+ *               three all-to-allv (ids, reply lengths, reply lists); the
+ *               requester intersects N_v with each reply.  data_sent /
+ *               data_recv = requests + replies.  Refused when a rank's reply
+ *               lists would not fit its device.
  * Every rank returns the same total, per_rank (nranks) and boundaries
  * (nranks+1); cfg->ranks must be 0 or nranks; cfg->boundaries overrides
  * the plan. */

@@ -107,19 +107,21 @@ def graph_from_rows(n: int, row_lo: int, row_hi: int, offsets, adj, degrees,
 
 
 def split_rows(off: np.ndarray, parts: int) -> np.ndarray:
-    """parts+1 row boundaries splitting a CSR into equal adjacency volume,
-    rounded to whole 32-vertex tiles (the default input distribution; tile-
-    aligned rows orient with the one-pass tile kernel)."""
+    """parts+1 row boundaries splitting a CSR into equal orientation cost
+    (adjacency entries + 32 per row, the library's own split: csrc/comm.cu
+    k_volume_split), rounded to whole 32-vertex tiles (the default input
+    distribution; tile-aligned rows orient with the one-pass tile kernel)."""
     n = off.shape[0] - 1
-    tgt = (np.arange(parts + 1, dtype=np.float64) * float(off[-1]) / parts)
-    b = np.searchsorted(off, tgt, side="left").astype(np.uint64) & ~np.uint64(31)
+    cost = off.astype(np.float64) + 32.0 * np.arange(n + 1, dtype=np.float64)
+    tgt = (np.arange(parts + 1, dtype=np.float64) * float(cost[-1]) / parts)
+    b = np.searchsorted(cost, tgt, side="left").astype(np.uint64) & ~np.uint64(31)
     b[0], b[-1] = 0, n
     return np.maximum.accumulate(np.minimum(b, n)).astype(np.uint32)
 
 
 def run_engine_comm(g: Graph, comm: Comm, cfg: Optional[EngineConfig] = None) -> RunReport:
-    """run_engine across the communicator (tg_run_engine_comm): Aop or
-    AnopSurrogate counts; every rank returns the same report."""
+    """run_engine across the communicator (tg_run_engine_comm): Aop,
+    AnopDirect or AnopSurrogate counts; every rank returns the same report."""
     p = comm.size
     cfg = cfg or EngineConfig(engine=EngineKind.Aop, ranks=p)
     c, keep = _cfg(EngineConfig(engine=cfg.engine, ranks=p, cost=cfg.cost, order=cfg.order,

@@ -22,6 +22,9 @@
 //                computed from distributed costs, each rank's oriented rows
 //                move to their core owner with one all-to-allv (Σ stored = m),
 //                then the surrogate all-to-allv and the counts;
+//   DIRECT    -- (engines.hpp:80-141) the same core partitions; one request
+//                per off-core pair (v, u) to owner(u), one reply carrying
+//                N_u, batched into three all-to-allv;
 //   tallies   -- per-rank n-vectors reduced to their owner's core range
 //                (one NCCL reduce per owner in a group), C_v at the owner.
 // The global count is one all-reduce of a u64; per-rank stats are gathered
@@ -228,19 +231,24 @@ struct LocalTransport : Transport {
 
 // ------------------------------------------------------------------ kernels
 
+constexpr uint64_t kRowCost = 32;
 __global__ void k_volume_split(const uint64_t* __restrict__ off, uint64_t n, uint32_t parts,
                                uint32_t* __restrict__ a) {
-  // a[j] = smallest v with off[v] >= j * off[n] / parts (a[0] = 0, a[parts] = n),
+  // Equal ORIENTATION COST: c(v) = off[v] + kRowCost v -- a row costs what ~32
+  // adjacency entries do (fit of the per-rank orientation times of C5 at
+  // N = 8, profiles/r02h_scaling.jsonl: 6.05e-9 ms per entry + 1.91e-7 ms per
+  // row; an equal-adjacency split left the last rank at 2.1x the first).
+  // a[j] = smallest v with c(v) >= j * c(n) / parts (a[0] = 0, a[parts] = n),
   // rounded down to whole 32-vertex tiles (the tile kernel's unit)
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j > parts) return;
   if (j == 0) { a[0] = 0; return; }
   if (j == parts) { a[parts] = (uint32_t)n; return; }
-  const unsigned __int128 target = (unsigned __int128)off[n] * j;
+  const unsigned __int128 target = (unsigned __int128)(off[n] + kRowCost * n) * j;
   uint64_t lo = 0, hi = n;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
-    if ((unsigned __int128)off[mid] * parts >= target) hi = mid;
+    if ((unsigned __int128)(off[mid] + kRowCost * mid) * parts >= target) hi = mid;
     else lo = mid + 1;
   }
   a[j] = (uint32_t)(lo & ~31ull);
@@ -323,6 +331,91 @@ __global__ void k_cc_range(const uint32_t* __restrict__ deg, const unsigned long
   }
 }
 
+// ---- ANOP-direct (engines.hpp:80-141): request / reply kernels ----
+__device__ __forceinline__ uint32_t owner_dev(const uint32_t* __restrict__ gb, uint32_t p, uint32_t u) {
+  uint32_t lo = 0, hi = p;  // the i with gb[i] <= u < gb[i+1] (partition.hpp:104-109)
+  while (lo + 1 < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (gb[mid] <= u) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One request per off-core entry u of a core list N_v (the reference sends
+// one per (v, u) pair and never caches): FILL = false counts them per owner,
+// FILL = true writes (u, v) destination-major at the cursors.
+template <bool FILL>
+__global__ void __launch_bounds__(256)
+k_direct_requests(CsrView part, uint32_t cb, uint32_t ce, const uint32_t* __restrict__ gb, uint32_t p,
+                  uint32_t self, unsigned long long* __restrict__ cnt_or_cur,
+                  uint32_t* __restrict__ req_u, uint32_t* __restrict__ req_v) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < ce - cb; w += warps) {
+    const uint64_t d = part.desc[w];
+    const uint32_t* L = part.data + desc_start(d);
+    for (uint32_t i = lane; i < desc_len(d); i += 32) {
+      const uint32_t u = L[i], ou = owner_dev(gb, p, u);
+      if (ou == self) continue;
+      const unsigned long long pos = atomicAdd(&cnt_or_cur[ou], 1ull);
+      if (FILL) {
+        req_u[pos] = u;
+        req_v[pos] = cb + (uint32_t)w;
+      }
+    }
+  }
+}
+
+// serve_request (engines.hpp:93-99): the length of each requested core list
+__global__ void k_reply_lens(CsrView part, const uint32_t* __restrict__ got_u, uint64_t R,
+                             uint32_t* __restrict__ lens) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < R;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    lens[i] = desc_len(part.desc[got_u[i] - part.base]);
+}
+
+// ... and the lists themselves, back to back in request order
+__global__ void __launch_bounds__(256)
+k_reply_fill(CsrView part, const uint32_t* __restrict__ got_u, uint64_t R,
+             const uint64_t* __restrict__ off, uint32_t* __restrict__ payload) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
+    const uint64_t d = part.desc[got_u[i] - part.base];
+    const uint32_t* L = part.data + desc_start(d);
+    for (uint32_t k = lane; k < desc_len(d); k += 32) payload[off[i] + k] = L[k];
+  }
+}
+
+// the requester's intersect_visit(N_v, reply) (engines.hpp:121-126): a warp
+// per reply, each element searched in the sorted core list N_v
+__global__ void __launch_bounds__(256)
+k_direct_count(CsrView part, const uint32_t* __restrict__ req_v, uint64_t R,
+               const uint64_t* __restrict__ off, const uint32_t* __restrict__ payload,
+               unsigned long long* __restrict__ total) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long acc = 0;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
+    const uint64_t d = part.desc[req_v[i] - part.base];
+    const uint32_t* Nv = part.data + desc_start(d);
+    const uint32_t hv = desc_len(d);
+    for (uint64_t k = off[i] + lane; k < off[i + 1]; k += 32) {
+      const uint32_t x = payload[k];
+      uint32_t a = 0, b = hv;
+      while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (Nv[mid] < x) a = mid + 1;
+        else b = mid;
+      }
+      acc += a < hv && Nv[a] == x;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0 && acc) atomicAdd(total, acc);
+}
+
 template <class F>
 void cub_run(cudaStream_t s, F&& f) {
   size_t bytes = 0;
@@ -386,7 +479,7 @@ std::vector<uint64_t> all_gather_host(Transport& T, const std::vector<uint64_t>&
 }
 
 // The rows this rank orients: its own rows (rank-local graph; the ranks'
-// ranges must tile [0, n) in rank order) or an equal-adjacency-volume split.
+// ranges must tile [0, n) in rank order) or an equal-orientation-cost split.
 std::vector<uint32_t> row_split(tg_graph* g, Transport& T) {
   const uint32_t N = (uint32_t)T.size;
   cudaStream_t s = g->stream;
@@ -807,8 +900,9 @@ tg_status tg_run_engine_comm(tg_graph* g, tg_comm* c, const tg_config* cfg, uint
   return guard([&] {
     tgh::enter(g);
     TG_REQUIRE(c && cfg, "null argument");
-    TG_REQUIRE(cfg->engine == TG_ENGINE_AOP || cfg->engine == TG_ENGINE_ANOP_SURROGATE,
-               "across ranks: Aop and AnopSurrogate");
+    TG_REQUIRE(cfg->engine == TG_ENGINE_AOP || cfg->engine == TG_ENGINE_ANOP_SURROGATE ||
+                   cfg->engine == TG_ENGINE_ANOP_DIRECT,
+               "across ranks: Aop, AnopDirect and AnopSurrogate");
     TG_REQUIRE(cfg->cost >= TG_COST_N && cfg->cost <= TG_COST_NOV, "unknown cost kind");
     TG_REQUIRE(!cfg->sparsify && !cfg->track_nodes && !cfg->collect_triangles,
                "across ranks: counts only (tallies via tg_clustering_comm)");
@@ -842,8 +936,9 @@ tg_status tg_run_engine_comm(tg_graph* g, tg_comm* c, const tg_config* cfg, uint
       gather_costs(g, T, o, TG_COST_DPD, f, s);
       mine.realized_cost = core_sums(f, n, b, s)[r];
     } else {
-      // ANOP-surrogate: lengths + distributed costs -> plan; oriented rows
-      // to their core owner (partition.hpp:210-239); surrogate exchange
+      // ANOP (direct or surrogate): lengths + distributed costs -> plan;
+      // oriented rows to their core owner (partition.hpp:210-239); then the
+      // engine's exchange
       orient_mine(g, T, o);
       DBuf<uint64_t> f;
       if (cfg->boundaries) {
@@ -893,6 +988,105 @@ tg_status tg_run_engine_comm(tg_graph* g, tg_comm* c, const tg_config* cfg, uint
         part.desc.alloc(1, s);
       }
       mine.stored_entries = part.entries;
+      if (cfg->engine == TG_ENGINE_ANOP_DIRECT) {
+        // anop_direct_body (engines.hpp:80-141), batched: every off-core pair
+        // (v, u) is one request to owner(u) and one reply carrying N_u; the
+        // requester intersects N_v with each reply.  Three exchanges: the
+        // requested ids, the reply lengths, the reply lists.
+        const CsrView pv = tgh::view(part);
+        const CountOut out{ctr.p, nullptr, nullptr, nullptr, 0};
+        DBuf<uint32_t> gb(N + 1, s);
+        TG_CUDA(cudaMemcpyAsync(gb.p, b.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
+        DBuf<unsigned long long> cur(N, s);
+        cur.zero();
+        const unsigned grid = tgb::grid_for((uint64_t)(ce - cb) * 32, 256, 148u * 16u);
+        if (ce > cb) {
+          tgb::k_direct_requests<false><<<grid, 256, 0, s>>>(pv, cb, ce, gb.p, (uint32_t)N,
+                                                             (uint32_t)r, cur.p, nullptr, nullptr);
+          TG_CHECK_LAUNCH();
+          ++tgb::g_launches;
+        }
+        std::vector<uint64_t> cnt(N, 0);
+        TG_CUDA(cudaMemcpyAsync(cnt.data(), cur.p, N * 8, cudaMemcpyDeviceToHost, s));
+        TG_CUDA(cudaStreamSynchronize(s));
+        auto all_cnt = all_gather_host(T, cnt, s);  // [i][j] = requests from i to j
+        std::vector<uint64_t> start(N + 1, 0), rstart(N + 1, 0);
+        std::vector<size_t> sq(N), rq(N);
+        for (int j = 0; j < N; ++j) {
+          start[j + 1] = start[j] + cnt[j];
+          rstart[j + 1] = rstart[j] + all_cnt[(size_t)j * N + r];
+          sq[j] = cnt[j] * 4;
+          rq[j] = all_cnt[(size_t)j * N + r] * 4;
+        }
+        const uint64_t Rs = start[N], Rr = rstart[N];  // requests sent / received
+        DBuf<uint32_t> req_u(Rs + 1, s), req_v(Rs + 1, s), got_u(Rr + 1, s);
+        TG_CUDA(cudaMemcpyAsync(cur.p, start.data(), N * 8, cudaMemcpyHostToDevice, s));
+        if (ce > cb) {
+          tgb::k_direct_requests<true><<<grid, 256, 0, s>>>(pv, cb, ce, gb.p, (uint32_t)N,
+                                                            (uint32_t)r, cur.p, req_u.p, req_v.p);
+          TG_CHECK_LAUNCH();
+          ++tgb::g_launches;
+        }
+        T.all_to_allv(req_u.p, sq, got_u.p, rq, s);
+        // replies: lengths first (their sizes are the request counts, reversed)
+        DBuf<uint32_t> my_lens(Rr + 1, s), rl(Rs + 1, s);
+        if (Rr) {
+          tgb::k_reply_lens<<<tgb::grid_for(Rr, 256), 256, 0, s>>>(pv, got_u.p, Rr, my_lens.p);
+          TG_CHECK_LAUNCH();
+          ++tgb::g_launches;
+        }
+        T.all_to_allv(my_lens.p, rq, rl.p, sq, s);
+        auto scan = [&](const DBuf<uint32_t>& l, uint64_t cntl, DBuf<uint64_t>& off) {
+          off.alloc(cntl + 1, s);
+          TG_CUDA(cudaMemsetAsync(off.p, 0, 8, s));
+          if (!cntl) return;
+          DBuf<uint64_t> l64(cntl, s);
+          tgb::k_u32_to_u64<<<tgb::grid_for(cntl, 256), 256, 0, s>>>(l.p, cntl, l64.p);
+          TG_CHECK_LAUNCH();
+          tgb::cub_run(s, [&](void* t, size_t& bb) {
+            return cub::DeviceScan::InclusiveSum(t, bb, l64.p, off.p + 1, (int64_t)cntl, s);
+          });
+          tgb::g_launches += 2;
+        };
+        DBuf<uint64_t> soff, roff;  // reply offsets: the ones I serve, the ones I receive
+        scan(my_lens, Rr, soff);
+        scan(rl, Rs, roff);
+        std::vector<size_t> sp(N), rp(N);
+        for (int j = 0; j < N; ++j) {
+          sp[j] = (tgb::read_u64(soff.p + rstart[j + 1], s) - tgb::read_u64(soff.p + rstart[j], s)) * 4;
+          rp[j] = (tgb::read_u64(roff.p + start[j + 1], s) - tgb::read_u64(roff.p + start[j], s)) * 4;
+        }
+        const uint64_t sw = tgb::read_u64(soff.p + Rr, s), rw = tgb::read_u64(roff.p + Rs, s);
+        size_t mfree = 0, mtot = 0;
+        TG_CUDA(cudaMemGetInfo(&mfree, &mtot));
+        TG_REQUIRE((sw + rw) * 4 + (64ull << 20) < mfree,
+                   "AnopDirect: the reply lists of this rank do not fit the device (one list per "
+                   "off-core pair, engines.hpp:80-141); use AnopSurrogate");
+        DBuf<uint32_t> pay(sw + 1, s), rpay(rw + 1, s);
+        if (Rr) {
+          tgb::k_reply_fill<<<tgb::grid_for(Rr * 32, 256, 148u * 16u), 256, 0, s>>>(pv, got_u.p, Rr,
+                                                                                  soff.p, pay.p);
+          TG_CHECK_LAUNCH();
+          ++tgb::g_launches;
+        }
+        T.all_to_allv(pay.p, sp, rpay.p, rp, s);
+        if (ce > cb) {
+          // in-core pairs locally, off-core pairs against their replies
+          tgb::intersect_rows(pv, cb, ce, pv, cb, ce, out, g->scr, s, part.data.n, false);
+          if (Rs) {
+            tgb::k_direct_count<<<tgb::grid_for(Rs * 32, 256, 148u * 16u), 256, 0, s>>>(
+                pv, req_v.p, Rs, roff.p, rpay.p, ctr.p);
+            TG_CHECK_LAUNCH();
+            ++tgb::g_launches;
+          }
+        }
+        mine.triangles = tgb::read_u64((const uint64_t*)ctr.p, s);
+        mine.data_sent = Rs + Rr;  // requests sent + replies sent
+        mine.data_recv = Rr + Rs;  // requests received + replies received
+        DBuf<uint64_t> fd;
+        gather_costs(g, T, o, TG_COST_DPD, fd, s);
+        mine.realized_cost = core_sums(fd, n, b, s)[r];
+      } else {
       // SurrogatePack (engines.hpp:173-187) + the exchange of (v, N_v)
       tgb::SurrogatePack pack;
       pack.build(tgh::view(part), cb, ce, b, (uint32_t)r, s);
@@ -936,6 +1130,7 @@ tg_status tg_run_engine_comm(tg_graph* g, tg_comm* c, const tg_config* cfg, uint
       DBuf<uint64_t> fn;
       gather_costs(g, T, o, TG_COST_NOV, fn, s);
       mine.realized_cost = core_sums(fn, n, b, s)[r];
+      }
     }
     auto st = all_gather_host(
         T, {mine.triangles, mine.data_sent, mine.data_recv, mine.realized_cost, mine.stored_entries},

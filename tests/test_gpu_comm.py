@@ -71,6 +71,7 @@ def test_engines_across_ranks(graph, nranks, local_rows):
     rows = M.split_rows(ref.off, nranks)
     want_aop = O.run_engine(ref, "aop", nranks, "DPD")
     want_sur = O.run_engine(ref, "anop-surrogate", nranks, "DPD")
+    want_dir = O.run_engine(ref, "anop-direct", nranks, "DPD")
     want_T, want_tv, _ = O.count(ref, tally=True)
     want_cc = O.clustering(ref, want_tv)
 
@@ -78,17 +79,24 @@ def test_engines_across_ranks(graph, nranks, local_rows):
         g = rank_graph(ref, pairs, rows, r, local_rows)
         a = M.run_engine_comm(g, comm, T.EngineConfig(engine=T.EngineKind.Aop))
         s = M.run_engine_comm(g, comm, T.EngineConfig(engine=T.EngineKind.AnopSurrogate))
+        dr = M.run_engine_comm(g, comm, T.EngineConfig(engine=T.EngineKind.AnopDirect))
         b, tv, cc = M.clustering_comm(g, comm)
         d = torch.zeros(1, dtype=torch.int64, device="cuda")
         M.aop_step_comm(g, comm, a.boundaries, d.data_ptr())
         torch.cuda.synchronize()
         step = int(d.item())
         g.close()
-        return a, s, (b, tv, cc), step
+        return a, s, (b, tv, cc), step, dr
 
     res = run_ranks(nranks, body)
-    for r, (a, s, (b, tv, cc), step) in enumerate(res):
-        assert a.total == want_T == s.total == step
+    for r, (a, s, (b, tv, cc), step, dr) in enumerate(res):
+        assert a.total == want_T == s.total == step == dr.total
+        # ANOP-direct (engines.hpp:80-141): request / reply data path
+        assert dr.boundaries.tolist() == want_dir.boundaries[:nranks + 1].tolist()
+        assert [x.triangles for x in dr.per_rank] == want_dir.triangles[:nranks].tolist()
+        assert [x.data_sent for x in dr.per_rank] == want_dir.data_sent[:nranks].tolist()
+        assert [x.data_recv for x in dr.per_rank] == want_dir.data_recv[:nranks].tolist()
+        assert sum(x.stored_entries for x in dr.per_rank) == ref.m
         assert a.boundaries.tolist() == want_aop.boundaries[:nranks + 1].tolist()
         assert [x.triangles for x in a.per_rank] == want_aop.triangles[:nranks].tolist()
         assert [x.stored_entries for x in a.per_rank] == want_aop.stored[:nranks].tolist()

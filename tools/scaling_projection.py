@@ -2,7 +2,7 @@
 """Per-rank work of the N-GPU AOP step (csrc/comm.cu tg_aop_step_comm),
 measured rank by rank on ONE B200, and the projected N-GPU step.
 
-The step at N GPUs: rank r orients ONLY its rows (an equal-adjacency-volume
+The step at N GPUs: rank r orients ONLY its rows (an equal-orientation-cost
 split, effective.hpp:37-52), the oriented rows of all ranks are broadcast in
 rank order over NVLink (list lengths first: 4 B per vertex), and the rank
 counts the apexes of its DPD core (engines.hpp:38-54, partition.hpp:116-141)
@@ -14,9 +14,14 @@ Modelled (one GPU per call in this environment):
   xfer_r    -- bytes rank r receives (others' oriented entries + lengths)
                at NVLINK_GBS (an assumption, stated in the output);
   + one 8-byte all-reduce (30 us).
-Projected step = max_r(orient_r + xfer_r + count_r) (serial) and
-max_r(orient_r + max(xfer_r, count_r)) (the count overlapped with the
-broadcasts, as tg_aop_step_comm schedules it -- an upper bound on overlap).
+  slab_r    -- on PA-like graphs (mean list > 16) every rank fills the n
+               slabs from the gathered lists as the slices arrive (slab_rows:
+               4 m + 128 n bytes streamed) at SLAB_GBS (an assumption too);
+  + one 8-byte all-reduce (30 us).
+Projected step = max_r(orient_r + xfer_r + slab_r + count_r) (serial) and
+max_r(orient_r + max(xfer_r, slab_r + count_r)) (slab fill and count
+overlapped with the broadcasts, as tg_aop_step_comm schedules them -- an
+upper bound on overlap).
 
     python tools/scaling_projection.py C2 [C5] [--nvlink-gbs 700]
 """
@@ -45,6 +50,8 @@ def main():
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--nvlink-gbs", type=float, default=700.0,
                     help="assumed NCCL broadcast bandwidth per receiving GPU (GB/s)")
+    ap.add_argument("--slab-gbs", type=float, default=5000.0,
+                    help="assumed streaming rate of slab_rows (GB/s)")
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     L = lib()
@@ -94,14 +101,15 @@ def main():
                                                                            dp))))
                 ranks.append([lo, hi, t_or, t_ct])
             tot = sum(cnts)
+            slab_ms = ((4 * m + 128 * n) / (a.slab_gbs * 1e9) * 1e3) if m > 16 * n else 0.0
             out = []
             for r, (lo, hi, t_or, t_ct) in enumerate(ranks):
                 rx = (tot - cnts[r]) * 4 + (n - (hi - lo)) * 4
                 t_x = rx / (a.nvlink_gbs * 1e9) * 1e3
                 out.append({"rows": [lo, hi], "orient_ms": t_or, "count_ms": t_ct,
-                            "recv_bytes": rx, "xfer_ms": t_x,
-                            "serial_ms": t_or + t_x + t_ct + ALLREDUCE_MS,
-                            "overlap_ms": t_or + max(t_x, t_ct) + ALLREDUCE_MS})
+                            "recv_bytes": rx, "xfer_ms": t_x, "slab_ms": slab_ms,
+                            "serial_ms": t_or + t_x + slab_ms + t_ct + ALLREDUCE_MS,
+                            "overlap_ms": t_or + max(t_x, slab_ms + t_ct) + ALLREDUCE_MS})
             ser = max(x["serial_ms"] for x in out)
             ovl = max(x["overlap_ms"] for x in out)
             rec["N"][N] = {"ranks": out, "step_serial_ms": ser, "step_overlap_ms": ovl,
