@@ -598,6 +598,8 @@ def run_ours(args):
 
 
 def main():
+    # one JSON line on stdout: NCCL's own messages (its version banner) go to stderr
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
