@@ -121,6 +121,7 @@ k_intersect_ctab(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
         for (uint32_t ch0 = t >> 5; ch0 < nch; ch0 += kCWarps * kCQUnroll) {
           uint4 r[kCQUnroll];
           uint32_t jjs[kCQUnroll], vms[kCQUnroll], qix[kCQUnroll];
+          unsigned full = 0;  // chunks with all 128 slots valid (warp-uniform bits)
 #pragma unroll
           for (int q = 0; q < kCQUnroll; ++q) {
             const uint32_t ch = ch0 + q * kCWarps;
@@ -130,8 +131,21 @@ k_intersect_ctab(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             qix[q] = 0;
             if (ch < nch) {  // warp-uniform
               const uint32_t word = sTbl[ch], nxt = sTbl[ch + 1];
-              const uint32_t jj = sPre[ch] + __popc(word & le_mask) - 1u;
               const uint32_t idx = w0 + 32 * ch + lane;
+              if ((word | (nxt & 1u)) == 0u && w0 + 32 * ch + 32 <= wend) {
+                // interior chunk (warp-uniform): 32 whole quads of ONE list, no
+                // segment start or end inside -- the common case on the hub
+                // lists this path reads (ncu on C3: the per-quad segment / mask
+                // bookkeeping was 45% of the kernel's instructions)
+                const uint32_t jj = sPre[ch] - 1u;
+                jjs[q] = jj;
+                qix[q] = sQs[jj] + idx;
+                r[q] = ldg_cq4(R4 + qix[q]);
+                vms[q] = 0xFu;
+                full |= 1u << q;
+                continue;
+              }
+              const uint32_t jj = sPre[ch] + __popc(word & le_mask) - 1u;
               jjs[q] = jj;
               if (idx < wend) {
                 qix[q] = sQs[jj] + idx;
@@ -152,12 +166,20 @@ k_intersect_ctab(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             // values: masked slots probe bit 0 instead
             const uint32_t xr[4] = {r[q].x, r[q].y, r[q].z, r[q].w};
             unsigned hb = 0;
+            if ((full >> q) & 1u) {
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-              const uint32_t xo = ((vms[q] >> s2) & 1u) ? xr[s2] - base : 0u;
-              hb |= ((sBits[xo >> 5] >> (xo & 31)) & 1u) << s2;
+              for (int s2 = 0; s2 < 4; ++s2) {
+                const uint32_t xo = xr[s2] - base;
+                hb |= ((sBits[xo >> 5] >> (xo & 31)) & 1u) << s2;
+              }
+            } else {
+#pragma unroll
+              for (int s2 = 0; s2 < 4; ++s2) {
+                const uint32_t xo = ((vms[q] >> s2) & 1u) ? xr[s2] - base : 0u;
+                hb |= ((sBits[xo >> 5] >> (xo & 31)) & 1u) << s2;
+              }
+              hb &= vms[q];
             }
-            hb &= vms[q];
             apex_cnt += __popc(hb);
             if (TALLY || LIST) {
 #pragma unroll

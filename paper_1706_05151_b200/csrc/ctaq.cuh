@@ -154,8 +154,16 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
             vms[q] = 0;
             if (ch < nch) {  // warp-uniform
               const uint32_t word = sTbl[ch], nxt = sTbl[ch + 1];
-              const uint32_t jj = sPre[ch] + __popc(word & le_mask) - 1u;
               const uint32_t idx = w0 + 32 * ch + lane;
+              if ((word | (nxt & 1u)) == 0u && w0 + 32 * ch + 32 <= wend) {
+                // interior chunk (warp-uniform): 32 whole quads of one list
+                const uint32_t jj = sPre[ch] - 1u;
+                jjs[q] = jj;
+                r[q] = ldg_cq4(Q4 + (sQs[jj] + idx));
+                vms[q] = 0xFu;
+                continue;
+              }
+              const uint32_t jj = sPre[ch] + __popc(word & le_mask) - 1u;
               jjs[q] = jj;
               if (idx < wend) {
                 r[q] = ldg_cq4(Q4 + (sQs[jj] + idx));
