@@ -262,9 +262,6 @@ constexpr int kOTbl = 32;       // table window: 1024 items
 constexpr int kOUnroll = TG_OUNROLL;
 constexpr int kOBlocks = TG_OBLOCKS;  // resident blocks per SM (launch bounds, grid)
 
-#ifndef TG_SLAB_STAGE
-#define TG_SLAB_STAGE 0
-#endif
 constexpr uint32_t kOBig = 256;  // degree above which a vertex leaves its tile
 constexpr uint32_t kOHub = 4096;  // ... and above which a whole CTA orients it (ONE mode)
 
@@ -294,11 +291,6 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
   __shared__ uint32_t sV[kOWarps][32], sDv[kOWarps][32], sSt[kOWarps][32], sSh[kOWarps][32];
   __shared__ uint32_t sCum[kOWarps][32], sAs[kOWarps][32];
   __shared__ uint32_t sHb[SLAB ? kOWarps : 1][32];  // kept entries of the tile before a segment
-#if TG_SLAB_STAGE
-  // the tile's 32 slabs staged in shared memory and written out as whole
-  // 128-byte lines (no global pad prefill, no 4-byte scattered stores)
-  __shared__ __align__(16) uint32_t sSlab[SLAB ? kOWarps : 1][SLAB ? 32 * kSlab : 4];
-#endif
   constexpr bool FILL = MODE == 1, ONE = MODE == 2;
   static_assert(!SLAB || ONE, "the slab layout is written by the one-pass mode");
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -320,11 +312,6 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
     const uint32_t len = (uint32_t)(my_e - my_b);
     const bool big = len > kOBig;
     if (SLAB) {  // pad the tile's 32 slabs (4 KB, 8 coalesced 16-byte stores per lane)
-#if TG_SLAB_STAGE
-      uint4* Q = reinterpret_cast<uint4*>(sSlab[w]);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) Q[32 * j + lane] = make_uint4(kNoEntry, kNoEntry, kNoEntry, kNoEntry);
-#else
       uint4* Q = reinterpret_cast<uint4*>(eff);
       const uint64_t qend = n * (kSlab / 4);
 #pragma unroll
@@ -332,7 +319,6 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
         const uint64_t qi = v0 * (kSlab / 4) + 32 * j + lane;
         if (qi < qend) Q[qi] = make_uint4(kNoEntry, kNoEntry, kNoEntry, kNoEntry);
       }
-#endif
       __syncwarp();  // ordered before the entries written below
     }
     if (!FILL && !ONE && big) bigq[atomicAdd(bigq_n, 1ull)] = (uint32_t)v;
@@ -355,19 +341,6 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
         else if (!FILL) cnt_or_eoff[v] = 0;
         else edesc[v] = make_desc(cnt_or_eoff[v], 0);
       }
-#if TG_SLAB_STAGE
-      if (SLAB) {  // all pads
-        uint4* G = reinterpret_cast<uint4*>(eff);
-        const uint4* Q = reinterpret_cast<const uint4*>(sSlab[w]);
-        const uint64_t qend = n * (kSlab / 4);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint64_t qi = v0 * (kSlab / 4) + 32 * j + lane;
-          if (qi < qend) G[qi] = Q[32 * j + lane];
-        }
-        __syncwarp();
-      }
-#endif
       continue;
     }
     // FILL: tile-relative output base of each segment, minus its items before
@@ -472,11 +445,7 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
               if (idx < wend && idx == sst) sHb[w][jj] = before;
               __syncwarp();
               const uint32_t r = before - sHb[w][jj & 31u];  // (idle lanes: any slot)
-#if TG_SLAB_STAGE
-              if (keep && r < kSlab) sSlab[w][(sv - (uint32_t)v0) * kSlab + r] = us[q];
-#else
               if (keep && r < kSlab) eff[(uint64_t)sv * kSlab + r] = us[q];
-#endif
             } else if (ONE && keep) eff[tile_b + kept + __popc(km & lt_mask)] = us[q];
             if (!ONE && lane == 0 && km) {  // record the decisions for the FILL pass
               const uint64_t pos = tile_b + base;
@@ -491,18 +460,6 @@ k_orient_tiles(const uint64_t* __restrict__ off, const uint32_t* __restrict__ ad
       __syncwarp();
     }
     __syncwarp();
-#if TG_SLAB_STAGE
-    if (SLAB) {  // the staged slabs, as whole lines
-      uint4* G = reinterpret_cast<uint4*>(eff);
-      const uint4* Q = reinterpret_cast<const uint4*>(sSlab[w]);
-      const uint64_t qend = n * (kSlab / 4);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint64_t qi = v0 * (kSlab / 4) + 32 * j + lane;
-        if (qi < qend) G[qi] = Q[32 * j + lane];
-      }
-    }
-#endif
     if (!FILL && valid && !big) {
       uint32_t h = 0, hb = 0;
       if (elen > 0) {
