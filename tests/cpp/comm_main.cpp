@@ -1,7 +1,7 @@
 // One C++ host driving N ranks through the C ABI (csrc/comm.cu): a thread
 // per rank, each with its rank-local rows of the graph (tg_graph_from_rows),
-// running run_engine across the ranks (AOP and ANOP-surrogate,
-// engines.hpp:38-54, 146-198), the AOP step and clustering at the owners.
+// running run_engine across the ranks (AOP, ANOP-direct and ANOP-surrogate,
+// engines.hpp:38-54, 80-141, 146-198), the AOP step and clustering at the owners.
 // Checked against the single-device count of the whole graph.
 //
 //   comm_main <nranks> [local|nccl]
@@ -71,7 +71,7 @@ int main(int argc, char** argv) {
     std::vector<int> devs(N, 0);
     CK(tg_comm_init_local(N, devs.data(), comms.data()));
   }
-  std::vector<uint64_t> aop(N), sur(N), step(N), stored(N), tsum(N);
+  std::vector<uint64_t> aop(N), sur(N), dir(N), step(N), stored(N), tsum(N);
   std::vector<int> ok(N, 0);
   std::vector<std::thread> th;
   for (int r = 0; r < N; ++r)
@@ -86,6 +86,16 @@ int main(int argc, char** argv) {
       std::vector<tg_rank_stats> st(N);
       std::vector<uint32_t> b(N + 1);
       CK(tg_run_engine_comm(g, comms[r], &cfg, &aop[r], st.data(), b.data()));
+      // ANOP-direct (engines.hpp:80-141): request / reply data path; as many
+      // requests + replies sent as received over the whole job
+      cfg.engine = TG_ENGINE_ANOP_DIRECT;
+      CK(tg_run_engine_comm(g, comms[r], &cfg, &dir[r], st.data(), nullptr));
+      uint64_t ds = 0, dr = 0;
+      for (int i = 0; i < N; ++i) {
+        ds += st[i].data_sent;
+        dr += st[i].data_recv;
+      }
+      if (ds != dr) dir[r] = ~0ull;
       cfg.engine = TG_ENGINE_ANOP_SURROGATE;
       CK(tg_run_engine_comm(g, comms[r], &cfg, &sur[r], st.data(), nullptr));
       stored[r] = 0;
@@ -109,7 +119,7 @@ int main(int argc, char** argv) {
   for (auto& t : th) t.join();
   int failures = 0;
   for (int r = 0; r < N; ++r) {
-    if (!ok[r] || aop[r] != want || sur[r] != want || step[r] != want || tsum[r] != want ||
+    if (!ok[r] || aop[r] != want || sur[r] != want || dir[r] != want || step[r] != want || tsum[r] != want ||
         stored[r] != m) {
       std::printf("FAIL rank %d: aop %llu sur %llu step %llu per-rank sum %llu stored %llu "
                   "(want %llu, m %llu)\n",
