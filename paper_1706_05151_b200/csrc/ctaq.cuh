@@ -21,6 +21,10 @@
 #define TG_CQUNROLL 4
 #endif
 constexpr int kCQUnroll = TG_CQUNROLL;  // quad chunks in flight per warp (ctaq, ctab)
+#ifndef TG_CPH_MAX
+#define TG_CPH_MAX 256
+#endif
+constexpr uint32_t kCPhMax = TG_CPH_MAX;  // longest N_v tried as a perfect hash (<= kCT)
 
 template <bool TALLY, bool LIST, bool FILTER, class Apex>
 __global__ void __launch_bounds__(kCT, 2)
@@ -53,6 +57,12 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
   if (nbig > big_cap) nbig = big_cap;
   const uint32_t tcap = 1u << tcap_log2;
   unsigned long long acc = 0;
+  // Perfect-hash mode (round 2, as in slab.cuh): an N_v of <= kCPhMax keys goes
+  // into the table region as a direct-mapped table under the first of 8
+  // multipliers that maps its keys to distinct slots; a probe is then one
+  // LDS + compare, exact -- no filter, no hit queue, no second search.  The
+  // region is kept all-empty between apexes (`dirty` after a hash-set apex).
+  bool dirty = true;
 
   for (;;) {
     if (t == 0) sItem = atomicAdd(work_ctr, 1ull);
@@ -67,9 +77,32 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       __syncthreads();  // sItem is rewritten at the loop top
       continue;
     }
+    bool use_ph = false;
+    uint32_t pmul = 0, pslot = 0;
+    const uint32_t psh = 32u - tcap_log2;
+    if (hv <= kCPhMax && tcap >= 4096u) {
+      if (dirty) {
+        for (uint32_t i = t; i < tcap; i += kCT) sHt[i] = kCEmpty;
+        dirty = false;
+        __syncthreads();
+      }
+      const uint32_t x = t < hv ? L[t] : kCEmpty;  // one key per thread (kCPhMax <= kCT)
+      for (int tr = 0; tr < 8; ++tr) {
+        pmul = ph_mul(tr);
+        pslot = (x * pmul) >> psh;
+        if (t < hv) sHt[pslot] = x;
+        __syncthreads();
+        if (__syncthreads_and(t >= hv || sHt[pslot] == x)) {
+          use_ph = true;
+          break;
+        }
+        if (t < hv) sHt[pslot] = kCEmpty;
+        __syncthreads();
+      }
+    }
     uint32_t bits = 3;
     while ((1u << bits) < hv) ++bits;
-    bool in_ht = (4u << bits) <= tcap;
+    bool in_ht = !use_ph && (4u << bits) <= tcap;
     const Ht4 H{sHt, 32u - bits};
     // inverted blocked filter, 16 bits per key (>= 32 words)
     uint32_t bmb = bits + 4;
@@ -78,15 +111,18 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
     uint32_t* Bm = sHt + tcap;
     const uint32_t wshift = 32 - (bmb - 5), bwords = 1u << (bmb - 5);
     if (t == 0) sOvf = 0;
-    for (uint32_t i = t; i < bwords; i += kCT) Bm[i] = 0xFFFFFFFFu;
-    if (in_ht)
-      for (uint32_t i = t; i < (4u << bits); i += kCT) sHt[i] = kCEmpty;
-    __syncthreads();
-    for (uint32_t i = t; i < hv; i += kCT) {
-      const uint32_t x = L[i];
-      if (in_ht && !H.insert(x)) sOvf = 1;
-      const uint32_t h = bm_hash(x);
-      atomicAnd(&Bm[h >> wshift], ~qm_mask(h));
+    if (!use_ph) {
+      dirty = dirty || in_ht;
+      for (uint32_t i = t; i < bwords; i += kCT) Bm[i] = 0xFFFFFFFFu;
+      if (in_ht)
+        for (uint32_t i = t; i < (4u << bits); i += kCT) sHt[i] = kCEmpty;
+      __syncthreads();
+      for (uint32_t i = t; i < hv; i += kCT) {
+        const uint32_t x = L[i];
+        if (in_ht && !H.insert(x)) sOvf = 1;
+        const uint32_t h = bm_hash(x);
+        atomicAnd(&Bm[h >> wshift], ~qm_mask(h));
+      }
     }
     if (t == 0) {
       sApex = 0;
@@ -180,6 +216,34 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
 #pragma unroll
           for (int q = 0; q < kCQUnroll; ++q) {
             const uint32_t xq[4] = {r[q].x, r[q].y, r[q].z, r[q].w};
+            if (use_ph) {  // (block-uniform) exact probes, no queue
+              unsigned fb = 0;
+#pragma unroll
+              for (int s2 = 0; s2 < 4; ++s2)
+                fb |= (unsigned)(sHt[(xq[s2] * pmul) >> psh] == xq[s2]) << s2;
+              fb &= vms[q];
+              apex_cnt += __popc(fb);
+              if (TALLY || LIST) {
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) {
+                  const bool found = (fb >> s2) & 1u;
+                  if (TALLY && found) {
+                    atomicAdd(&out.tally[xq[s2]], 1ull);
+                    atomicAdd(&sCntU[jjs[q]], 1u);
+                  }
+                  if (LIST) {
+                    const unsigned m = __ballot_sync(FULL, found);
+                    if (m) {
+                      unsigned long long b0 = 0;
+                      if (lane == 0) b0 = atomicAdd(out.cursor, (unsigned long long)__popc(m));
+                      b0 = __shfl_sync(FULL, b0, 0);
+                      if (found) emit_triple(out, b0 + __popc(m & lt_mask), v, sU[jjs[q]], xq[s2]);
+                    }
+                  }
+                }
+              }
+              continue;
+            }
             // filter (branch-free), then enqueue the hits (warp-aggregated)
             unsigned hb = 0;
 #pragma unroll
@@ -237,6 +301,7 @@ k_intersect_ctaq(Apex A, CsrView nu, uint32_t ulo, uint32_t uhi, CountOut out,
       if (TALLY && sApex) atomicAdd(&out.tally[v], sApex);
       acc += sApex;
     }
+    if (use_ph && t < hv) sHt[pslot] = kCEmpty;  // the table region stays all-empty
     __syncthreads();
   }
   if (t == 0 && acc) atomicAdd(out.total, acc);
