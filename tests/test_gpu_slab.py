@@ -116,6 +116,41 @@ def test_slab_with_nibble_codes(slab, graph):
         slab.tg_debug_set_paths(0, 0)
 
 
+def test_slab_next_rows(slab):
+    """SURVEY 8(f) rows over the slab layout: sparsified engines
+    (sparsify.hpp, engines.hpp:335-457: they read the oriented lists through
+    their descriptors), per-edge counts (sequential.hpp:108-122, the LIST sink
+    of the slab kernel) and the non-degree orders"""
+    pairs = T.gen_pa(4000, 44, 8)
+    ref = O.build_graph(pairs)
+    slab.tg_debug_set_slab(1)
+    g = T.build_graph(pairs, ref.n)
+    assert T.count_node_iterator_n(g) == O.count(ref)[0]
+    assert np.array_equal(T.per_edge_triangle_counts(g), O.per_edge_counts(ref))
+    modes = {"global": T.SparsifyMode.Global, "per-partition": T.SparsifyMode.PerPartition}
+    engines = {"seq": T.EngineKind.Sequential, "aop": T.EngineKind.Aop,
+               "anop-direct": T.EngineKind.AnopDirect, "anop-surrogate": T.EngineKind.AnopSurrogate}
+    for eng, kind in engines.items():
+        for mode, mk in modes.items():
+            p = 1 if eng == "seq" else 4
+            want = O.run_engine(ref, eng, p, "DPD", sparsify=mode, q=0.6, seed=77,
+                                track_nodes=True, collect_triangles=True)
+            got = T.run_engine(g, T.EngineConfig(engine=kind, ranks=p, track_nodes=True,
+                                                 collect_triangles=True,
+                                                 sparsify=T.SparsifyConfig(0.6, 77, mk)))
+            assert got.total == want.total, (eng, mode)
+            assert [r.triangles for r in got.per_rank] == want.triangles.tolist()
+            assert [r.data_sent for r in got.per_rank] == want.data_sent.tolist()
+            assert np.array_equal(got.node_counts, want.node_counts)
+    for eng in ("aop", "anop-direct", "anop-surrogate"):
+        want = O.run_engine(ref, eng, 5, "DPD")
+        got = T.run_engine(g, T.EngineConfig(engine=engines[eng], ranks=5))
+        assert [r.triangles for r in got.per_rank] == want.triangles.tolist(), eng
+        assert [r.data_sent for r in got.per_rank] == want.data_sent.tolist(), eng
+        assert [r.stored_entries for r in got.per_rank] == want.stored.tolist(), eng
+    g.close()
+
+
 def test_slab_quad_kernel_on_slab_layout(slab):
     """the descriptor-driven kernels read the slab layout too (variant sweep)"""
     pairs = T.gen_pa(20000, 50, 11)
